@@ -1,0 +1,199 @@
+/*
+ * triadcensus.h -- C ABI of libtriadcensus.so, the B200 (sm_100a) directed
+ * triad census of arXiv 1603.02655 (Batagelj-Mrvar subquadratic algorithm).
+ *
+ * Citations: "P:n" = PAPER.md line n (the thesis LaTeX), "S:n" = SPEC.md.
+ *
+ * What is computed.  For a strict digraph G = [V, E], V = {0..n-1},
+ * counts[k-1] is the number of unordered vertex triples whose induced
+ * sub-digraph is isomorphic to class k, in the paper's order:
+ *   k:  1    2    3    4    5    6    7    8    9    10   11  12   13   14   15  16
+ *      003  012  102  021D 021U 021C 111D 111U 030T 030C 201 120D 120U 120C 210 300
+ * The device computes classes 2..16 by the B-M loop of Fig. "Subquadratic
+ * Triad Census Algorithm": for every canonical connected dyad
+ * u < v it adds n - |S| - 2 dyadic triads, S = N(u) U N(v) \ {u,v}, to class
+ * 3 (mutual dyad) or 2 (asymmetric), and classifies each canonical w in S
+ * (predicate P:292: v < w or (u < w < v and w not adjacent to u)) through
+ * the 64-code TriadCode (v0.4 form P:1396-1432) and the 64->16
+ * TriadTable.  Class 1 is closed on the host as
+ * n(n-1)(n-2)/6 - sum in 128-bit arithmetic.
+ *
+ * Conventions.
+ *  - Vertex ids are 0-based uint32; n must satisfy 0 <= n < 2^30 (ids are
+ *    packed as (w<<2)|tag in the device CSR) else TC_E_INVALID.
+ *  - Self-loops are dropped and duplicate arcs merged (strict digraph,
+ *    P:239/P:264); both are counted in tc_graph_stats.
+ *  - m (arcs given) must be < 2^31 and the number of distinct connected
+ *    dyads D < 2^31, else TC_E_INVALID.
+ *  - "Canonical dyad index" k numbers the connected unordered pairs {u,v},
+ *    u < v, in the algorithm's own order: u ascending, then v ascending
+ *    (S:312-320).  tc_census_range and sharding use it.
+ *  - Class 003 can exceed 2^64 (n > 4,801,280): its high word is returned
+ *    separately.  Every other class fits in uint64.
+ *  - All functions return tc_status; nothing throws across the ABI.  On
+ *    error, tc_last_error() gives a message (thread-local, valid until the
+ *    next call on that thread).
+ *  - Device work is issued on the caller's CUDA stream (cudaStream_t passed
+ *    as void*; NULL = legacy default stream).  tc_graph_create, tc_census,
+ *    tc_census_range and tc_census_multi return after the stream has drained
+ *    (results on the host); tc_census_enqueue does not synchronise.
+ *  - A tc_graph may be shared read-only by concurrent census calls on
+ *    different streams.
+ */
+#ifndef TRIADCENSUS_H
+#define TRIADCENSUS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TC_ABI_VERSION 1
+
+typedef struct tc_graph tc_graph;
+typedef struct tc_comm tc_comm;
+
+typedef enum {
+    TC_OK = 0,
+    TC_E_INVALID = 1,   /* bad argument (NULL pointer, n >= 2^30, size limits) */
+    TC_E_RANGE = 2,     /* an arc endpoint >= n; tc_last_error names the arc index */
+    TC_E_OOM = 3,       /* device allocation failed */
+    TC_E_CUDA = 4,      /* CUDA runtime error; message holds cudaGetErrorString */
+    TC_E_NCCL = 5,      /* NCCL error or NCCL library not loadable */
+    TC_E_OVERFLOW = 6   /* c003_hi == NULL but the 003 count needs a high word */
+} tc_status;
+
+/* Device memory hook.  alloc(bytes, stream, ctx) returns a device pointer
+ * usable on `stream` (or NULL on failure); free(ptr, bytes, stream, ctx)
+ * releases it.  Pass NULL for the default (cudaMallocAsync/cudaFreeAsync on
+ * the call's stream).  The Python binding passes torch's caching allocator. */
+typedef struct {
+    void *(*alloc)(size_t bytes, void *stream, void *ctx);
+    void (*free)(void *ptr, size_t bytes, void *stream, void *ctx);
+    void *ctx;
+} tc_allocator;
+
+/* Graph statistics after sanitising (a1 of SURVEY.md section 8(a)). */
+typedef struct {
+    uint64_t n;             /* vertices, including isolated ones */
+    uint64_t m_in;          /* arcs given */
+    uint64_t m;             /* distinct arcs after loop drop + dedup */
+    uint64_t loops_dropped;
+    uint64_t dups_dropped;
+    uint64_t dyads;         /* D: connected unordered pairs (canonical dyads) */
+    uint64_t mutual_dyads;  /* pairs with both arcs */
+    uint64_t max_degree;    /* Delta = max |N(u)| (undirected degree) */
+    uint64_t sum_deg_sq;    /* sum_u |N(u)|^2 = sum over canonical dyads of |N(u)|+|N(v)| */
+} tc_graph_stats;
+
+/* Per-phase device times (ms, CUDA events on the call's stream) of the most
+ * recent tc_graph_create / census call on this graph, when profiling is on. */
+typedef struct {
+    float build_ms;         /* a1: sort + dedup + symmetrise + offsets + stats */
+    float plan_ms;          /* a2: per-dyad cost and degree bins */
+    float census_ms;        /* a3+a4: all bin kernels incl. histogram flush */
+    float kernel_ms[4];     /* a3+a4 per bin: [0] thread, [1] warp, [2] block, [3] spare */
+    uint64_t bin_items[4];  /* dyads (or dyad chunks for the block bin) per bin */
+    uint64_t bin_work[4];   /* sum of |N(u)|+|N(v)| per bin */
+} tc_profile;
+
+/* Build the device graph from an arc list (a1).
+ *   device          CUDA device ordinal.
+ *   n               number of vertices (explicit: isolated vertices count).
+ *   src, dst        m arc endpoints (arc i is src[i] -> dst[i]); host
+ *                   pointers if arcs_on_device == 0 (copied H2D inside the
+ *                   call), else device pointers (only read).  Borrowed.
+ *   cuda_stream     cudaStream_t or NULL.
+ *   alloc           allocator hook or NULL.
+ *   out             receives the graph; owned by the caller, release with
+ *                   tc_graph_destroy.
+ * Layout built: uint32 off[n+1]; uint32
+ * adj[2D] with entry (w<<2)|tag, rows sorted by w, tag bit0 = u->w,
+ * bit1 = w->u (P:458-469 adjacency array, symmetric and tagged); uint32
+ * dyad lists of the canonical entries.
+ * Errors: TC_E_INVALID, TC_E_RANGE (first offending arc index in the
+ * message), TC_E_OOM, TC_E_CUDA. */
+tc_status tc_graph_create(int device, uint64_t n, const uint32_t *src, const uint32_t *dst,
+                          uint64_t m, int arcs_on_device, void *cuda_stream,
+                          const tc_allocator *alloc, tc_graph **out);
+
+tc_status tc_graph_stats_get(const tc_graph *g, tc_graph_stats *out);
+
+/* Frees every device buffer of the graph (stream-ordered on the creating
+ * stream).  NULL is a no-op. */
+void tc_graph_destroy(tc_graph *g);
+
+/* Full census (a2..a5), synchronous.
+ *   counts   host uint64[16]; counts[k-1] = class k, counts[0] = low word of 003.
+ *   c003_hi  host uint64 receiving the high word of the 003 count; may be
+ *            NULL only if that word is 0, else TC_E_OVERFLOW (counts still
+ *            filled). */
+tc_status tc_census(const tc_graph *g, void *cuda_stream, uint64_t counts[16],
+                    uint64_t *c003_hi);
+
+/* Partial census over canonical dyads [dyad_begin, dyad_end) (clamped to
+ * [0, D)): classes 2..16 only, partial[0] = 0.  Partials over any partition
+ * of [0, D) sum to the full census minus 003.  Synchronous. */
+tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
+                          void *cuda_stream, uint64_t partial[16]);
+
+/* Asynchronous partial census: enqueues a2..a4 for dyads [dyad_begin,
+ * dyad_end) on the stream and ADDS classes 2..16 into the device array
+ * d_counts[16] (uint64, caller-owned, caller zeroes it).  No host sync,
+ * no closing.  The plan's bin sizes are read back, so the call does wait
+ * once for the (small) plan counts. */
+tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
+                            void *cuda_stream, uint64_t *d_counts);
+
+/* Host closing (a5): counts[0], *c003_hi = C(n,3) - sum(counts[1..15]) in
+ * 128-bit.  Returns TC_E_INVALID if the sum exceeds C(n,3). */
+tc_status tc_close_census(uint64_t n, uint64_t counts[16], uint64_t *c003_hi);
+
+/* Degree-balanced shard cuts: splits canonical
+ * dyads [0, D) into `world` contiguous ranges of near-equal uniform cost
+ * sum(|N(u)| + |N(v)| + kappa) (the paper's uniform workload, P:1693,
+ * P:1837, applied across GPUs).  bounds[r], bounds[r+1] delimit rank r;
+ * bounds must hold world+1 entries.  Host-only pure function over host
+ * `cost` (per-dyad |N(u)|+|N(v)|, length D); the device path applies the
+ * same rule to its device cost prefix. */
+tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint64_t kappa,
+                               uint64_t *bounds);
+
+/* Same cut rule on the device graph (bounds for every rank, host array of
+ * world+1 entries). */
+tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds);
+
+/* NCCL communicator.  Rank 0 calls tc_comm_unique_id, the 128 bytes are
+ * broadcast by the caller (e.g. torch.distributed), then every rank calls
+ * tc_comm_create.  NCCL is loaded lazily (libnccl.so.2, the copy torch
+ * loaded if present); TC_E_NCCL if unavailable. */
+tc_status tc_comm_unique_id(uint8_t id[128]);
+tc_status tc_comm_create(const uint8_t id[128], int world, int rank, int device, tc_comm **out);
+void tc_comm_destroy(tc_comm *c);
+
+/* Multi-GPU census: each rank holds the full graph (replicated CSR),
+ * computes its degree-balanced shard of canonical dyads, and the 16 partial
+ * counts are summed by one ncclAllReduce (uint64, sum) on the stream.  Every
+ * rank receives the identical full census (closing done after the
+ * reduction).  Synchronous. */
+tc_status tc_census_multi(const tc_graph *g, tc_comm *comm, void *cuda_stream,
+                          uint64_t counts[16], uint64_t *c003_hi);
+
+/* Profiling: when on, every build / census records CUDA events around its
+ * phases on the call's stream (adds one host sync per call). */
+tc_status tc_profile_enable(tc_graph *g, int on);
+tc_status tc_profile_get(const tc_graph *g, tc_profile *out);
+
+/* Number of device kernels the last census/build call launched (for the
+ * bench's gpu_launches claim). */
+uint64_t tc_launch_count(const tc_graph *g);
+
+const char *tc_last_error(void);
+int tc_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TRIADCENSUS_H */

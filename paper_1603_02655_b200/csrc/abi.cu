@@ -1,0 +1,428 @@
+// abi.cu -- the C ABI of libtriadcensus.so (include/triadcensus.h): argument
+// checks, device/stream/allocator plumbing, the host closing (a5) and the
+// NCCL multi-GPU census.  No census arithmetic lives here beyond the 128-bit
+// null-triad closing n(n-1)(n-2)/6 - sum.
+#include <dlfcn.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+
+#include "census.cuh"
+
+namespace tc {
+
+static thread_local std::string g_err;
+
+void set_error(const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+tc_status cuda_status(cudaError_t e, const char *what) {
+    set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+    return e == cudaErrorMemoryAllocation ? TC_E_OOM : TC_E_CUDA;
+}
+
+void *Mem::alloc(size_t bytes) {
+    if (bytes == 0) bytes = 1;
+    if (custom) return hook.alloc(bytes, (void *)stream, hook.ctx);
+    void *p = nullptr;
+    if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void Mem::free(void *p, size_t bytes) {
+    if (!p) return;
+    if (bytes == 0) bytes = 1;
+    if (custom) hook.free(p, bytes, (void *)stream, hook.ctx);
+    else cudaFreeAsync(p, stream);
+}
+
+// ---- 128-bit closing (a5) ------------------------------------------------
+static unsigned __int128 choose3(uint64_t n) {
+    if (n < 3) return 0;   // DESIGN.md reading 18
+    return (unsigned __int128)n * (n - 1) * (n - 2) / 6;
+}
+
+}  // namespace tc
+
+using namespace tc;
+
+extern "C" {
+
+const char *tc_last_error(void) { return g_err.c_str(); }
+int tc_abi_version(void) { return TC_ABI_VERSION; }
+
+tc_status tc_close_census(uint64_t n, uint64_t counts[16], uint64_t *c003_hi) {
+    if (!counts) {
+        set_error("counts is NULL");
+        return TC_E_INVALID;
+    }
+    unsigned __int128 sum = 0;
+    for (int k = 1; k < 16; k++) sum += counts[k];
+    unsigned __int128 total = choose3(n);
+    if (sum > total) {
+        set_error("census sum exceeds C(n,3): internal inconsistency");
+        return TC_E_INVALID;
+    }
+    unsigned __int128 c1 = total - sum;
+    counts[0] = (uint64_t)c1;
+    uint64_t hi = (uint64_t)(c1 >> 64);
+    if (c003_hi) *c003_hi = hi;
+    else if (hi) {
+        set_error("the 003 count needs a high word (n > 4,801,280) but c003_hi is NULL");
+        return TC_E_OVERFLOW;
+    }
+    return TC_OK;
+}
+
+tc_status tc_graph_create(int device, uint64_t n, const uint32_t *src, const uint32_t *dst,
+                          uint64_t m, int arcs_on_device, void *cuda_stream,
+                          const tc_allocator *alloc, tc_graph **out) {
+    if (!out) {
+        set_error("out is NULL");
+        return TC_E_INVALID;
+    }
+    *out = nullptr;
+    if (n >= (1ull << 30)) {
+        set_error("n = %llu must be < 2^30", (unsigned long long)n);
+        return TC_E_INVALID;
+    }
+    if (m >= (1ull << 31)) {
+        set_error("m = %llu must be < 2^31", (unsigned long long)m);
+        return TC_E_INVALID;
+    }
+    if (m && (!src || !dst)) {
+        set_error("src/dst is NULL");
+        return TC_E_INVALID;
+    }
+    if (alloc && (!alloc->alloc || !alloc->free)) {
+        set_error("allocator hook has NULL functions");
+        return TC_E_INVALID;
+    }
+    TC_CUDA(cudaSetDevice(device));
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    tc_graph *g = new tc_graph();
+    g->device = device;
+    g->stream = s;
+    g->mem.stream = s;
+    if (alloc) {
+        g->mem.custom = true;
+        g->mem.hook = *alloc;
+    }
+    g->st.n = n;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    tc_status st = TC_OK;
+    const uint32_t *ds = src, *dd = dst;
+    DevBuf<uint32_t> hs, hd;
+    if (!arcs_on_device && m) {
+        if ((st = hs.allocate(g->mem, m)) != TC_OK || (st = hd.allocate(g->mem, m)) != TC_OK) {
+            delete g;
+            return st;
+        }
+        cudaError_t e = cudaMemcpyAsync(hs.p, src, m * 4, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(hd.p, dst, m * 4, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) {
+            hs.release();
+            hd.release();
+            delete g;
+            return cuda_status(e, "H2D arc copy");
+        }
+        ds = hs.p;
+        dd = hd.p;
+    }
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    st = build_csr(g, ds, dd, m, s);
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) == cudaSuccess)
+        cudaEventElapsedTime(&g->prof.build_ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    hs.release();
+    hd.release();
+    if (st != TC_OK) {
+        std::string keep = g_err;
+        tc_graph_destroy(g);
+        g_err = keep;
+        return st;
+    }
+    *out = g;
+    return TC_OK;
+}
+
+tc_status tc_graph_stats_get(const tc_graph *g, tc_graph_stats *out) {
+    if (!g || !out) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    *out = g->st;
+    return TC_OK;
+}
+
+void tc_graph_destroy(tc_graph *g) {
+    if (!g) return;
+    cudaSetDevice(g->device);
+    g->mem.free(g->off, g->off_n * 4);
+    g->mem.free(g->adj, g->adj_n * 4);
+    g->mem.free(g->dyad_u, g->dyad_n * 4);
+    g->mem.free(g->dyad_p, g->dyad_n * 4);
+    cudaStreamSynchronize(g->stream);
+    delete g;
+}
+
+tc_status tc_profile_enable(tc_graph *g, int on) {
+    if (!g) {
+        set_error("NULL graph");
+        return TC_E_INVALID;
+    }
+    g->profile = on;
+    return TC_OK;
+}
+
+tc_status tc_profile_get(const tc_graph *g, tc_profile *out) {
+    if (!g || !out) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    *out = g->prof;
+    return TC_OK;
+}
+
+uint64_t tc_launch_count(const tc_graph *g) { return g ? g->launches : 0; }
+
+tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
+                            void *cuda_stream, uint64_t *d_counts) {
+    if (!g || !d_counts) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    TC_CUDA(cudaSetDevice(g->device));
+    tc_graph *mg = const_cast<tc_graph *>(g);
+    mg->launches = 0;
+    tc_profile *prof = g->profile ? &mg->prof : nullptr;
+    return census_range_device(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, d_counts, prof,
+                               &mg->launches);
+}
+
+static tc_status census_partial_sync(const tc_graph *g, uint64_t k0, uint64_t k1,
+                                     cudaStream_t s, uint64_t out[16]) {
+    TC_CUDA(cudaSetDevice(g->device));
+    Mem mem = g->mem;
+    mem.stream = s;
+    DevBuf<uint64_t> d;
+    tc_status st = d.allocate(mem, 16);
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(d.p, 0, 16 * sizeof(uint64_t), s));
+    if ((st = tc_census_enqueue(g, k0, k1, s, d.p)) != TC_OK) return st;
+    TC_CUDA(cudaMemcpyAsync(out, d.p, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    out[0] = 0;
+    return TC_OK;
+}
+
+tc_status tc_census(const tc_graph *g, void *cuda_stream, uint64_t counts[16], uint64_t *c003_hi) {
+    if (!g || !counts) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    tc_status st = census_partial_sync(g, 0, g->st.dyads, (cudaStream_t)cuda_stream, counts);
+    if (st != TC_OK) return st;
+    return tc_close_census(g->st.n, counts, c003_hi);
+}
+
+tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
+                          void *cuda_stream, uint64_t partial[16]) {
+    if (!g || !partial) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    return census_partial_sync(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, partial);
+}
+
+tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint64_t kappa,
+                               uint64_t *bounds) {
+    if (!bounds || world < 1 || world > 1024 || (D && !cost)) {
+        set_error("invalid shard arguments");
+        return TC_E_INVALID;
+    }
+    unsigned __int128 T = 0;
+    for (uint64_t k = 0; k < D; k++) T += cost[k] + kappa;
+    bounds[0] = 0;
+    bounds[world] = D;
+    // bounds[r] = first k whose exclusive cost prefix >= floor(T * r / world)
+    unsigned __int128 pre = 0;
+    uint64_t k = 0;
+    for (int r = 1; r < world; r++) {
+        unsigned __int128 t = T * (unsigned)r / (unsigned)world;
+        while (k < D && pre < t) {
+            pre += cost[k] + kappa;
+            k++;
+        }
+        bounds[r] = k;
+    }
+    return TC_OK;
+}
+
+tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds) {
+    if (!g || !bounds || world < 1 || world > 1024) {
+        set_error("invalid shard arguments");
+        return TC_E_INVALID;
+    }
+    TC_CUDA(cudaSetDevice(g->device));
+    return shard_bounds_device(g, world, (cudaStream_t)cuda_stream, kShardKappa, bounds);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// NCCL, loaded lazily so the library loads (and the CPU tests run) without it
+// ---------------------------------------------------------------------------
+namespace {
+
+typedef struct { char internal[128]; } nccl_uid;
+typedef void *nccl_comm_t;
+typedef int (*fn_get_uid)(nccl_uid *);
+typedef int (*fn_init_rank)(nccl_comm_t *, int, nccl_uid, int);
+typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t);
+typedef int (*fn_destroy)(nccl_comm_t);
+typedef const char *(*fn_errstr)(int);
+
+struct Nccl {
+    void *h = nullptr;
+    fn_get_uid get_uid = nullptr;
+    fn_init_rank init_rank = nullptr;
+    fn_allreduce allreduce = nullptr;
+    fn_destroy destroy = nullptr;
+    fn_errstr errstr = nullptr;
+};
+
+Nccl *nccl() {
+    static Nccl n;
+    static bool tried = false;
+    if (tried) return n.h ? &n : nullptr;
+    tried = true;
+    const char *names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char *nm : names) {
+        n.h = dlopen(nm, RTLD_NOW | RTLD_NOLOAD);   // the copy torch already loaded
+        if (!n.h) n.h = dlopen(nm, RTLD_NOW);
+        if (n.h) break;
+    }
+    if (!n.h) return nullptr;
+    n.get_uid = (fn_get_uid)dlsym(n.h, "ncclGetUniqueId");
+    n.init_rank = (fn_init_rank)dlsym(n.h, "ncclCommInitRank");
+    n.allreduce = (fn_allreduce)dlsym(n.h, "ncclAllReduce");
+    n.destroy = (fn_destroy)dlsym(n.h, "ncclCommDestroy");
+    n.errstr = (fn_errstr)dlsym(n.h, "ncclGetErrorString");
+    if (!n.get_uid || !n.init_rank || !n.allreduce || !n.destroy) {
+        n.h = nullptr;
+        return nullptr;
+    }
+    return &n;
+}
+
+const int kNcclUint64 = 5;   // ncclUint64 in nccl.h
+const int kNcclSum = 0;      // ncclSum
+
+tc_status nccl_fail(Nccl *n, int rc, const char *what) {
+    set_error("NCCL error %d (%s) in %s", rc, n && n->errstr ? n->errstr(rc) : "?", what);
+    return TC_E_NCCL;
+}
+
+}  // namespace
+
+struct tc_comm {
+    nccl_comm_t comm = nullptr;
+    int world = 1, rank = 0, device = 0;
+};
+
+extern "C" {
+
+tc_status tc_comm_unique_id(uint8_t id[128]) {
+    Nccl *n = nccl();
+    if (!n) {
+        set_error("libnccl.so.2 could not be loaded");
+        return TC_E_NCCL;
+    }
+    nccl_uid u;
+    int rc = n->get_uid(&u);
+    if (rc) return nccl_fail(n, rc, "ncclGetUniqueId");
+    memcpy(id, u.internal, 128);
+    return TC_OK;
+}
+
+tc_status tc_comm_create(const uint8_t id[128], int world, int rank, int device, tc_comm **out) {
+    if (!id || !out || world < 1 || rank < 0 || rank >= world) {
+        set_error("invalid communicator arguments");
+        return TC_E_INVALID;
+    }
+    Nccl *n = nccl();
+    if (!n) {
+        set_error("libnccl.so.2 could not be loaded");
+        return TC_E_NCCL;
+    }
+    TC_CUDA(cudaSetDevice(device));
+    nccl_uid u;
+    memcpy(u.internal, id, 128);
+    tc_comm *c = new tc_comm();
+    int rc = n->init_rank(&c->comm, world, u, rank);
+    if (rc) {
+        delete c;
+        return nccl_fail(n, rc, "ncclCommInitRank");
+    }
+    c->world = world;
+    c->rank = rank;
+    c->device = device;
+    *out = c;
+    return TC_OK;
+}
+
+void tc_comm_destroy(tc_comm *c) {
+    if (!c) return;
+    Nccl *n = nccl();
+    if (n && c->comm) n->destroy(c->comm);
+    delete c;
+}
+
+tc_status tc_census_multi(const tc_graph *g, tc_comm *comm, void *cuda_stream,
+                          uint64_t counts[16], uint64_t *c003_hi) {
+    if (!g || !comm || !counts) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    Nccl *n = nccl();
+    if (!n) {
+        set_error("libnccl.so.2 could not be loaded");
+        return TC_E_NCCL;
+    }
+    TC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    uint64_t bounds[1025];
+    tc_status st = shard_bounds_device(g, comm->world, s, kShardKappa, bounds);
+    if (st != TC_OK) return st;
+    Mem mem = g->mem;
+    mem.stream = s;
+    DevBuf<uint64_t> d;
+    if ((st = d.allocate(mem, 16)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(d.p, 0, 16 * sizeof(uint64_t), s));
+    if ((st = tc_census_enqueue(g, bounds[comm->rank], bounds[comm->rank + 1], s, d.p)) != TC_OK)
+        return st;
+    int rc = n->allreduce(d.p, d.p, 16, kNcclUint64, kNcclSum, comm->comm, s);
+    if (rc) return nccl_fail(n, rc, "ncclAllReduce");
+    TC_CUDA(cudaMemcpyAsync(counts, d.p, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    counts[0] = 0;
+    return tc_close_census(g->st.n, counts, c003_hi);
+}
+
+}  // extern "C"

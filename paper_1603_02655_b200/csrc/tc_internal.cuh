@@ -1,0 +1,116 @@
+// tc_internal.cuh -- internal declarations of libtriadcensus (not installed).
+//
+// Device data layout:
+//   off[n+1]   uint32 row offsets of the symmetric neighbour CSR
+//   adj[2D]    uint32 entries (w << 2) | tag, each row sorted by w;
+//              tag bit0 = u->w, bit1 = w->u (the 2-bit direction code)
+//   dyad_u[D], dyad_p[D]   canonical dyads (u < v) in canonical order
+//              (u ascending, v ascending): row u and the CSR
+//              position p of v in row u (so v = adj[p] >> 2, pre = adj[p] & 3)
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "triadcensus.h"
+
+namespace tc {
+
+// ---------------------------------------------------------------------------
+// errors
+// ---------------------------------------------------------------------------
+void set_error(const char *fmt, ...);
+tc_status cuda_status(cudaError_t e, const char *what);
+
+#define TC_CUDA(call)                                                          \
+    do {                                                                       \
+        cudaError_t _e = (call);                                               \
+        if (_e != cudaSuccess) return ::tc::cuda_status(_e, #call);            \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// stream-ordered device memory through the caller's allocator hook
+// ---------------------------------------------------------------------------
+struct Mem {
+    tc_allocator hook;
+    bool custom = false;
+    cudaStream_t stream = nullptr;
+    void *alloc(size_t bytes);
+    void free(void *p, size_t bytes);
+};
+
+template <typename T>
+struct DevBuf {
+    T *p = nullptr;
+    size_t n = 0;
+    Mem *mem = nullptr;
+    tc_status allocate(Mem &m, size_t count) {
+        mem = &m;
+        n = count;
+        size_t bytes = (count ? count : 1) * sizeof(T);
+        p = static_cast<T *>(m.alloc(bytes));
+        if (!p) {
+            set_error("device allocation of %zu bytes failed", bytes);
+            return TC_E_OOM;
+        }
+        return TC_OK;
+    }
+    void release() {
+        if (p && mem) mem->free(p, (n ? n : 1) * sizeof(T));
+        p = nullptr;
+        n = 0;
+    }
+    ~DevBuf() { release(); }
+};
+
+// ---------------------------------------------------------------------------
+// bin thresholds of the degree-binned scheduler (a2).  Cost c = |N(u)|+|N(v)|.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kThreadBinMax = 96;     // c <= 96: one thread per dyad
+constexpr uint32_t kWarpBinMax = 4096;     // c <= 4096: one warp per dyad
+constexpr uint32_t kBlockThreads = 256;    // block bin: 256 threads per chunk
+constexpr uint32_t kBlockSpan = 8192;      // diagonals per block-bin chunk
+constexpr int kNumBins = 3;
+// per-dyad overhead of the shard cost model, in list-entry equivalents
+// (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
+constexpr uint64_t kShardKappa = 8;
+
+struct BinItem2 {   // thread / warp bins
+    uint32_t u, p;
+};
+struct BinItem4 {   // block bin: dyad (u, p) and merge diagonals [d0, d1)
+    uint32_t u, p, d0, d1;
+};
+
+}  // namespace tc
+
+// the opaque graph
+struct tc_graph {
+    int device = 0;
+    cudaStream_t stream = nullptr;      // creating stream (used for frees)
+    tc::Mem mem;
+    tc_graph_stats st{};
+    uint32_t *off = nullptr;   size_t off_n = 0;
+    uint32_t *adj = nullptr;   size_t adj_n = 0;
+    uint32_t *dyad_u = nullptr; size_t dyad_n = 0;
+    uint32_t *dyad_p = nullptr;
+    int profile = 0;
+    tc_profile prof{};
+    uint64_t launches = 0;
+};
+
+namespace tc {
+
+// phase entry points (each file owns one step of SURVEY.md section 8(a))
+tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, uint64_t m,
+                    cudaStream_t s);                                  // a1, csr_build.cu
+tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
+                              uint64_t *d_counts, tc_profile *prof, uint64_t *launches);  // a2-a4
+tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
+                              uint64_t *bounds);                      // schedule.cu
+
+// generic device-wide exclusive scan with a per-element input functor and an
+// output functor; scan.cuh
+}  // namespace tc

@@ -1,0 +1,199 @@
+"""-m gpu: the CUDA path (through the C ABI) against the CPU oracle, element
+by element, bit-exact (integer counts, zero tolerance -- BASELINE.json
+north_star)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+NAMES = oracle.CLASS_NAMES
+
+
+@pytest.fixture(scope="module")
+def tcb():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1603_02655_b200 as m
+    return m
+
+
+def gpu_census(tcb, a):
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    try:
+        return g.census(), g.stats()
+    finally:
+        g.close()
+
+
+def vec(d):
+    return [int(d.get(k, 0)) for k in NAMES]
+
+
+def C3(n):
+    return n * (n - 1) * (n - 2) // 6 if n >= 3 else 0
+
+
+def test_single_triads(tcb):
+    for i, name in enumerate(NAMES):
+        a = synth.single_triad(name)
+        c, _ = gpu_census(tcb, a)
+        assert c == [1 if j == i else 0 for j in range(16)], name
+
+
+def test_spec_examples(tcb, golden_dir):
+    ex = json.load(open(os.path.join(golden_dir, "spec_examples.json")))
+    for e in ex["census"]:
+        arcs = np.array(e["arcs"], dtype=np.uint32).reshape(-1, 2)
+        a = synth.Arcs(e["n"], arcs[:, 0].copy(), arcs[:, 1].copy())
+        c, st = gpu_census(tcb, a)
+        for k, v in e["expect"].items():
+            assert c[NAMES.index(k)] == v, e["cite"]
+        for k, v in e.get("stats", {}).items():
+            assert st[k] == v, e["cite"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3])
+def test_tiny_orders(tcb, n):
+    a = synth.random_digraph(n, 0.9, seed=n, loops=True)
+    c, _ = gpu_census(tcb, a)
+    assert c == oracle.census(n, a.src, a.dst)
+
+
+def test_empty_and_loop_only(tcb):
+    a = synth.Arcs(10, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+    assert gpu_census(tcb, a)[0] == vec({"003": 120})
+    b = synth.Arcs(10, np.arange(10, dtype=np.uint32), np.arange(10, dtype=np.uint32))
+    c, st = gpu_census(tcb, b)
+    assert c == vec({"003": 120}) and st["loops_dropped"] == 10 and st["m"] == 0
+
+
+def test_random_graphs_vs_oracle(tcb):
+    rng = np.random.default_rng(0)
+    for s in range(120):
+        n = int(rng.integers(3, 400))
+        p = float(rng.choice([0.005, 0.02, 0.1, 0.4, 0.9]))
+        a = synth.random_digraph(n, p, seed=10_000 + s, loops=bool(s % 2), dups=s % 7)
+        c, st = gpu_census(tcb, a)
+        g = oracle.Graph(n, a.src, a.dst)
+        assert c == g.census(), (n, p, s)
+        assert st == g.stats(), (n, p, s)
+
+
+def test_C1_vs_bruteforce(tcb):
+    a = synth.make_config("C1")
+    c, _ = gpu_census(tcb, a)
+    assert c == oracle.bruteforce(a.n, a.src, a.dst)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_full_config_vs_golden(tcb, golden_dir, name):
+    rec = json.load(open(os.path.join(golden_dir, "census_%s.json" % name)))
+    a = synth.make_config(name)
+    c, st = gpu_census(tcb, a)
+    assert c == [int(x) for x in rec["census"]]
+    assert st == rec["stats"]
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_dyad_range_parity(tcb, name):
+    # T6: random canonical-dyad ranges, GPU partial == oracle partial
+    a = synth.make_config(name)
+    og = oracle.Graph(a.n, a.src, a.dst)
+    D = og.stats()["dyads"]
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    rng = np.random.default_rng(1)
+    for _ in range(4):
+        b = int(rng.integers(0, D))
+        e = min(D, b + int(rng.integers(1, 20_000)))
+        assert tcb.tc_census_range(g, b, e) == og.census_range(b, e), (b, e)
+    assert tcb.tc_census_range(g, D - 3, D + 100) == og.census_range(D - 3, D)
+    assert tcb.tc_census_range(g, 5, 5) == [0] * 16
+    g.close()
+
+
+def test_partials_sum_and_shard_bounds(tcb):
+    a = synth.make_config("C2")
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    full = g.census()
+    og = oracle.Graph(a.n, a.src, a.dst)
+    cost = og.dyad_costs()
+    for world in (1, 2, 3, 8):
+        b = tcb.tc_shard_bounds(g, world)
+        assert b == tcb.tc_shard_bounds_host(cost, world, kappa=8)
+        tot = [0] * 16
+        for r in range(world):
+            part = tcb.tc_census_range(g, b[r], b[r + 1])
+            tot = [x + y for x, y in zip(tot, part)]
+        assert tcb.tc_close_census(a.n, tot) == full
+    g.close()
+
+
+def test_relabelling_invariance(tcb):
+    a = synth.make_config("C2")
+    c, _ = gpu_census(tcb, a)
+    for seed in (5, 6):
+        assert gpu_census(tcb, synth.relabel(a, seed))[0] == c
+
+
+def test_device_arcs_equal_host_arcs(tcb):
+    import torch
+    a = synth.make_config("C2")
+    s = torch.from_numpy(a.src.astype(np.int32)).cuda()
+    d = torch.from_numpy(a.dst.astype(np.int32)).cuda()
+    g = tcb.tc_graph_create(a.n, s, d)
+    assert g.census() == gpu_census(tcb, a)[0]
+    g.close()
+
+
+def test_closed_form_hub_star_block_bin_and_high_word(tcb):
+    # cost 2e5+1 per dyad -> block bin; n = 1e7 -> 003 needs the high word
+    n, k = 10_000_000, 200_000
+    for gen, cp, cs in ((synth.out_star, "012", "021D"), (synth.mutual_star, "102", "201")):
+        a = gen(k, n)
+        exp = {cp: k * (n - k - 1), cs: k * (k - 1) // 2}
+        exp["003"] = C3(n) - sum(exp.values())
+        c, _ = gpu_census(tcb, a)
+        assert c == vec(exp)
+        assert c[0] >= 2**64
+
+
+def test_closed_form_tournament_clique_bipartite_cycle(tcb):
+    a = synth.transitive_tournament(3000)
+    assert gpu_census(tcb, a)[0] == vec({"030T": C3(3000)})
+    b = synth.complete_mutual(200)
+    assert gpu_census(tcb, b)[0] == vec({"300": C3(200)})
+    x, y = 4, 200_000
+    c = synth.complete_bipartite(x, y)
+    assert gpu_census(tcb, c)[0] == vec({"021U": y * 6, "021D": x * (y * (y - 1) // 2),
+                                         "003": C3(x) + C3(y)})
+    n = 1_000_000
+    d = synth.directed_cycle(n)
+    exp = {"012": n * (n - 4), "021C": n}
+    exp["003"] = C3(n) - sum(exp.values())
+    assert gpu_census(tcb, d)[0] == vec(exp)
+
+
+def test_mixed_bins_skewed_rmat(tcb):
+    # R-MAT scale 12 edge factor 16: dyads in thread, warp and block bins
+    a = synth.rmat(scale=12, edge_factor=16, seed=99)
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    g.profile(True)
+    c = g.census()
+    prof = g.profile_get()
+    assert c == oracle.census(a.n, a.src, a.dst)
+    assert all(x > 0 for x in prof["bin_items"][:2])
+    g.close()
+
+
+def test_errors(tcb):
+    with pytest.raises(tcb.TCError, match="arc 1 "):
+        tcb.tc_graph_create(5, np.array([0, 7, 1], np.uint32), np.array([1, 0, 2], np.uint32))
+    with pytest.raises(tcb.TCError, match="TC_E_INVALID"):
+        tcb.tc_graph_create(2**30, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
