@@ -1,0 +1,386 @@
+#!/usr/bin/env python
+"""bench.py -- directed triad census throughput on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl reference]
+
+One step = one pass of the whole hot path (SURVEY.md section 8(a) rows
+a1..a5) over the synthetic workload: GPU CSR build from the device-resident
+arc list (a1), degree-binned plan (a2), merge/classify kernels with the
+block histogram (a3+a4), closing (a5).  `value` = arcs processed by all ranks
+per second, timed with CUDA events on the launch stream, max over ranks.
+`e2e` = the same through the C ABI with HOST (pinned) arc buffers, the H2D
+copy and the result D2H inside the timed region.
+
+N > 1 (torchrun): every rank holds the replicated CSR, computes its
+degree-balanced dyad shard, and the 16 partial counts meet in one NCCL
+allreduce (tc_census_multi) -- strong scaling of one census.
+
+--impl reference: the CPU oracle (oracle/, plain single-threaded C) timed on
+the host on a bounded sample of the same workload; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "triad-census arcs/sec at 1/2/4/8 B200 (Patents-shaped); % HBM roofline"
+UNIT = "arcs/s"
+FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", default="C3")
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=15.0,
+                   help="bounded oracle sample for cpu_baseline")
+    return p.parse_args()
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        # one long-lived nvidia-smi sampling every 50 ms (our own child process)
+        try:
+            self._p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" +
+                                        self.FIELDS, "--format=csv,noheader,nounits",
+                                        "-lms", "50"], stdout=subprocess.PIPE,
+                                       stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            return
+        for line in self._p.stdout:
+            f = [x.strip() for x in line.strip().split(",")]
+            if len(f) >= 7:
+                self.samples.append(f)
+            if self._stop.is_set():
+                break
+
+    def __enter__(self):
+        self._p = None
+        self._t.start()
+        time.sleep(0.3)       # let the sampler start before the timed region
+        return self
+
+    def __exit__(self, *a):
+        time.sleep(0.1)
+        self._stop.set()
+        if self._p is not None:
+            self._p.terminate()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
+                    "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower().startswith("active")})
+        util = [float(s[6]) for s in self.samples if s[6].replace(".", "").isdigit()]
+        loaded = [c for c, u in zip(sm, util) if u > 0] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle baseline (rank 0, N = 1; and --impl reference)
+# ---------------------------------------------------------------------------
+def oracle_rate(a, seconds, steps=1):
+    """Time the oracle (as it stands) on a bounded sample: its graph build
+    (a1) once, then `steps` census samples, each a contiguous canonical-dyad
+    range sized to about `seconds`/steps of work, and extrapolate linearly
+    in the paper's uniform work units sum(|N(u)|+|N(v)|) to the whole census."""
+    import oracle
+    t0 = time.perf_counter()
+    g = oracle.Graph(a.n, a.src, a.dst)
+    t_build = time.perf_counter() - t0
+    cost = g.dyad_costs().astype(np.float64)
+    total = float(cost.sum()) or 1.0
+    pre = np.concatenate([[0.0], np.cumsum(cost)])
+    # calibrate: time a tiny range first
+    per_unit = None
+    k = 0
+    probe = int(np.searchsorted(pre, total * 0.002))
+    t0 = time.perf_counter()
+    g.census_range(0, max(probe, 1))
+    dt = time.perf_counter() - t0
+    per_unit = dt / max(pre[max(probe, 1)], 1.0)
+    k = max(probe, 1)
+    step_times, step_units = [], []
+    for _ in range(steps):
+        want = seconds / steps / max(per_unit, 1e-12)
+        e = int(np.searchsorted(pre, pre[k] + want))
+        e = min(max(e, k + 1), cost.size)
+        if k >= cost.size:
+            k = 0
+            e = min(int(np.searchsorted(pre, want)), cost.size)
+        t0 = time.perf_counter()
+        g.census_range(k, e)
+        dt = time.perf_counter() - t0
+        step_times.append(dt)
+        step_units.append(pre[e] - pre[k])
+        per_unit = dt / max(pre[e] - pre[k], 1.0)
+        k = e
+    rate_units = sum(step_units) / sum(step_times)
+    t_census_full = total / rate_units
+    t_full = t_build + t_census_full
+    frac = sum(step_units) / total
+    return {"value": a.m / t_full, "t_full_s": t_full, "t_build_s": t_build,
+            "t_census_full_s": t_census_full, "sample_frac": frac,
+            "step_times": step_times, "step_units": step_units, "total_units": total}
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return 0
+    a = synth.make_config(args.config)
+    steps = max(args.steps, 1)
+    per_step = max(2.0, min(8.0, 150.0 / (steps + args.warmup)))
+    r = oracle_rate(a, per_step * (steps + args.warmup), steps=steps + args.warmup)
+    times = r["step_times"][args.warmup:]
+    units = r["step_units"][args.warmup:]
+    rate_units = sum(units) / sum(times)
+    t_full = r["t_build_s"] + r["total_units"] / rate_units
+    value = a.m / t_full
+    sample = ("oracle build of the full graph once (%.1f s) + %d timed census samples of "
+              "contiguous canonical-dyad ranges (%.1f%% of sum(|N(u)|+|N(v)|) in total), "
+              "extrapolated linearly to the whole census" %
+              (r["t_build_s"], steps, 100 * sum(units) / r["total_units"]))
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": world, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": config_of(a, None),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(a, stats):
+    c = {"workload": "%s: %s" % (a.meta.get("config"), a.meta.get("label")),
+         "generator": a.meta.get("generator"), "seed": a.meta.get("seed"), "n": a.n,
+         "m_drawn": a.m}
+    if stats:
+        c.update({"m": stats["m"], "dyads": stats["dyads"], "sum_deg_sq": stats["sum_deg_sq"],
+                  "max_degree": stats["max_degree"]})
+    return c
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    rank, local, world = env_rank()
+    if world != args.gpus and not (world == 1 and args.gpus == 1):
+        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1603_02655_b200 as tcb
+
+    a = synth.make_config(args.config)
+    dev = torch.device("cuda", local)
+    s_dev = torch.from_numpy(a.src.view(np.int32)).to(dev)
+    d_dev = torch.from_numpy(a.dst.view(np.int32)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    comm = tcb.comm_from_process_group(local) if world > 1 else None
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def one_step(src, dst, profile=False):
+        g = tcb.tc_graph_create(a.n, src, dst, device=local, stream=stream)
+        launches = g.launches()
+        if profile:
+            g.profile(True)
+        counts = tcb.tc_census_multi(g, comm, stream) if comm else tcb.tc_census(g, stream)
+        launches += g.launches()
+        prof = g.profile_get() if profile else None
+        stats = g.stats()
+        g.close()
+        return counts, launches, prof, stats
+
+    # warm-up
+    ref_counts = None
+    for _ in range(args.warmup):
+        ref_counts, _, _, stats = one_step(s_dev, d_dev)
+    barrier()
+
+    # timed region: device-resident arcs
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches_total = 0
+    profs = []
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i)                       # L2 flush between steps (outside timing)
+            barrier()
+            ev[i][0].record(stream)
+            counts, nl, prof, stats = one_step(s_dev, d_dev, profile=True)
+            ev[i][1].record(stream)
+            launches_total += nl
+            profs.append(prof)
+            if ref_counts is not None:
+                assert counts == ref_counts, "census changed between steps"
+            ref_counts = counts
+        barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    total_ms = sum(step_ms)
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # e2e: host (pinned) arcs through the C ABI, H2D + D2H inside the region
+    s_host = torch.from_numpy(a.src.view(np.int32)).pin_memory()
+    d_host = torch.from_numpy(a.dst.view(np.int32)).pin_memory()
+    s_np = s_host.numpy().view(np.uint32)
+    d_np = d_host.numpy().view(np.uint32)
+    one_step(s_np, d_np)          # warm
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(i)
+        barrier()
+        t0 = time.perf_counter()
+        counts, _, _, _ = one_step(s_np, d_np)
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert counts == ref_counts
+    e2e_total = sum(e2e_ms)
+    if dist is not None:
+        t = torch.tensor([e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+
+    if rank != 0:
+        if dist is not None:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    # roofline of the dominant kernel (largest average bin-kernel time)
+    hbm, peak_src = peaks()
+    kms = np.array([p["kernel_ms"][:2] for p in profs])
+    avg_k = kms.mean(axis=0)
+    dom = int(np.argmax(avg_k))
+    # dyads and work per bin: thread bin = items[0]/work[0], warp bin = items[2]/work[1]
+    bin_dyads = [profs[-1]["bin_items"][0], profs[-1]["bin_items"][2]]
+    bin_work = [profs[-1]["bin_work"][0], profs[-1]["bin_work"][1]]
+    items = bin_dyads[dom]
+    work = bin_work[dom]
+    bytes_alg = 4.0 * work + 24.0 * items      # 4(du+dv)+24 B per dyad
+    achieved = bytes_alg / (avg_k[dom] * 1e-3) / 1e9
+    names = ["k_census_thread", "k_census_warp"]
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
+    if os.path.exists(tp):
+        tr = json.load(open(tp))
+        traffic = tr.get(names[dom])
+    census_ms = float(np.mean([p["census_ms"] for p in profs]))
+    plan_ms = float(np.mean([p["plan_ms"] for p in profs]))
+    build_ms = float(np.mean([p["build_ms"] for p in profs]))
+    sum_all_bins_bytes = 4.0 * sum(bin_work) + 24.0 * sum(bin_dyads)
+    m_arcs = a.m
+    line = {"metric": METRIC, "value": m_arcs * args.steps / (total_ms * 1e-3), "unit": UNIT,
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": dict(config_of(a, stats), **{
+                "l2": "inputs > L2 (arcs %.0f MB, sort keys %.0f MB) and a 512 MB L2 flush "
+                      "before every timed step" % (8 * a.m / 1e6, 32 * a.m / 1e6),
+                "step": "a1 build from device arcs + a2 plan + a3/a4 kernels + a5 closing",
+                "parallelism": "dp%d (replicated CSR, degree-balanced dyad shards, 1 NCCL "
+                               "allreduce)" % world if world > 1 else "single GPU"}),
+            "phases_ms": {"build": build_ms, "plan": plan_ms, "census_kernels": census_ms,
+                          "bin_kernels": [float(x) for x in avg_k],
+                          "census_arcs_per_s": m_arcs / ((plan_ms + census_ms) * 1e-3)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": names[dom],
+                         "bytes_alg_per_launch": bytes_alg,
+                         "peak_source": peak_src,
+                         "all_bins_frac": (sum_all_bins_bytes / (sum(avg_k) * 1e-3) / 1e9) / hbm},
+            "e2e": {"value": m_arcs * args.steps / (e2e_total * 1e-3), "unit": UNIT,
+                    "h2d_bytes_per_step": 8 * a.m, "d2h_bytes_per_step": 320},
+            "gpu_launches": launches_total,
+            "clocks": clk.summary(),
+            "census": [str(x) for x in ref_counts]}
+    if world == 1 and not args.no_cpu_baseline:
+        r = oracle_rate(a, args.cpu_seconds, steps=3)
+        line["cpu_baseline"] = {
+            "value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "oracle graph build once (%.1f s) + 3 contiguous canonical-dyad range "
+                      "censuses covering %.1f%% of sum(|N(u)|+|N(v)|), extrapolated linearly "
+                      "to the full census (%.1f s est.)" % (r["t_build_s"], 100 * r["sample_frac"],
+                                                             r["t_full_s"])}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -94,9 +94,9 @@ typedef struct {
     float build_ms;         /* a1: sort + dedup + symmetrise + offsets + stats */
     float plan_ms;          /* a2: per-dyad cost and degree bins */
     float census_ms;        /* a3+a4: all bin kernels incl. histogram flush */
-    float kernel_ms[4];     /* a3+a4 per bin: [0] thread, [1] warp, [2] block, [3] spare */
-    uint64_t bin_items[4];  /* dyads (or dyad chunks for the block bin) per bin */
-    uint64_t bin_work[4];   /* sum of |N(u)|+|N(v)| per bin */
+    float kernel_ms[4];     /* a3+a4 per bin: [0] thread bin, [1] warp bin, [2..3] 0 */
+    uint64_t bin_items[4];  /* [0] thread-bin dyads, [1] warp items, [2] warp-bin dyads */
+    uint64_t bin_work[4];   /* sum of |N(u)|+|N(v)|: [0] thread bin, [1] warp bin */
 } tc_profile;
 
 /* Build the device graph from an arc list (a1).
@@ -141,9 +141,8 @@ tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_
 
 /* Asynchronous partial census: enqueues a2..a4 for dyads [dyad_begin,
  * dyad_end) on the stream and ADDS classes 2..16 into the device array
- * d_counts[16] (uint64, caller-owned, caller zeroes it).  No host sync,
- * no closing.  The plan's bin sizes are read back, so the call does wait
- * once for the (small) plan counts. */
+ * d_counts[16] (uint64, caller-owned, caller zeroes it).  No host sync and
+ * no closing (unless profiling is on): bin sizes stay on the device. */
 tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                             void *cuda_stream, uint64_t *d_counts);
 

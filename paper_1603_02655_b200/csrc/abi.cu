@@ -176,7 +176,8 @@ void tc_graph_destroy(tc_graph *g) {
     g->mem.free(g->off, g->off_n * 4);
     g->mem.free(g->adj, g->adj_n * 4);
     g->mem.free(g->dyad_u, g->dyad_n * 4);
-    g->mem.free(g->dyad_p, g->dyad_n * 4);
+    g->mem.free(g->dyad_e, g->dyad_n * 4);
+    g->mem.free(g->dyad_c, g->dyad_n * 4);
     cudaStreamSynchronize(g->stream);
     delete g;
 }

@@ -2,34 +2,44 @@
 //
 // For a canonical dyad (u, v), u < v, with pre = tag of v in N(u)
 // (= IsEdge(u,v) + 2*IsEdge(v,u), the v0.4 pre-computed code),
-// the B-M loop body (Fig. P:269-309) is evaluated as one sorted merge of the
-// tagged rows A = N(u) and B = N(v):
+// the B-M loop body (Fig. P:269-309) is evaluated as ONE sorted merge of the
+// tagged rows A = N(u) and B = N(v) (entries (w<<2)|tag, sorted by w):
 //   * every merged id w is an element of N(u) U N(v); tu / tv are its tags in
-//     A / B (0 if absent), which are exactly IsEdge(u,w)+2*IsEdge(w,u) and
+//     A / B (0 if absent): exactly IsEdge(u,w)+2*IsEdge(w,u) and
 //     IsEdge(v,w)+2*IsEdge(w,v) of Fig. TriadCode;
 //   * line 16's predicate  v < w or (u < w < v and not IsNeighbour(u,w))
-//     becomes  (w > v) | (tu == 0 & w > u), which also rejects w = u (tu = 0,
-//     w = u) and w = v (w = v not > v, tu != 0);
+//     is, for w from A (tu != 0): w > v, and for w only in B (tu == 0):
+//     w > u; both reject w = u and w = v;
 //   * code = pre | tu<<2 | tv<<4 (bit weights 1,2,4,8,16,32 of P:329-347) and
-//     class = TriadTable[code], the 64-entry table held in shared
-//     memory (16 banks, no conflicts: all 64 entries share 16 words);
+//     class = TriadTable[code], looked up in shared memory (64 bytes:
+//     every lookup is conflict free);
 //   * the dyadic term n - |S| - 2 of line 14, with |S| = |N(u)|+|N(v)|-I-2
-//     (I = |N(u) & N(v)|), is accumulated as (n - du - dv) once per dyad plus
-//     one per intersection element, into class 3 (pre == 3, mutual) or 2.
-// The merge is split along merge-path diagonals so any number of threads can
-// share one dyad: a segment [d0, d1) starts at the merge-path split of d0
-// (ties go to A first; an equal pair is consumed together, so a segment that
-// starts right after a pair's A element skips the B element).
+//     (I = |N(u) & N(v)|), is added as (n - du - dv) once per dyad plus one
+//     per intersection element, to class 3 (pre == 3, mutual) or class 2.
 //
-// a4: per-thread 8-bit packed class counters (two uint64 registers, flushed
-// before they can overflow) -> per-block shared uint64[16] -> one global
-// atomicAdd per class per block.
+// Merge-path form: trip t consumes exactly one list element (A first on
+// equal ids), so a dyad of cost c = du + dv is exactly c trips; an
+// intersection element is classified when its A copy is consumed (both tags
+// are visible then) and its B twin is skipped.  A thread, a lane or a chunk
+// processes any diagonal range [d0, d1) after a merge-path split of d0.
+// Rows end in a sentinel (csr_build.cu), so the loop has no bounds checks,
+// the next element of each list is loaded one consumption ahead, and the
+// thread bin prefetches both rows into L2 when a dyad starts.
+// Thread-bin warps hold dyads of identical cost, so every lane runs the same
+// trip count (no divergence); warp items split one dyad over 32 lanes.
+//
+// a4: per thread, one uint64 of 16 4-bit class counters (+1 per trip at
+// nibble 4*class; non-canonical trips hit the unused nibble of class 003),
+// spilled every <= 15 trips into two uint64 of 8-bit counters (even / odd
+// classes), which a warp flushes (REDUX sum per class) into per-warp shared
+// totals before they can overflow; blocks end with one global atomicAdd per
+// class.
 #include "census.cuh"
 
 namespace tc {
 
 // TriadTable, 0-based classes in the paper's order 003..300.
-// Literal B-M 2001 TRICODES table minus one (reading 1); the
+// The literal B-M 2001 TRICODES table minus one (reading 1); the
 // oracle derives its own table by orbit enumeration and the tests compare.
 __constant__ uint8_t c_triad_table[64] = {
     0, 1, 1, 2, 1, 3, 5, 7, 1, 5, 4, 6, 2, 7, 6, 10, 1, 5, 3, 7, 4, 8, 8, 12, 5, 9, 8, 13, 6, 13, 11, 14,
@@ -37,36 +47,58 @@ __constant__ uint8_t c_triad_table[64] = {
 
 namespace {
 
+constexpr int kWarps = kCensusThreads / 32;
+constexpr uint64_t kNib = 0x0F0F0F0F0F0F0F0Full;
+
 struct Acc {
-    uint64_t lo, hi;      // 8-bit counters: classes 0..7 | 8..15 (0-based)
-    uint32_t pending;     // upper bound on increments since the last flush
+    uint64_t n4;            // 16 x 4-bit counters, nibble k = class k (0-based)
+    uint64_t ev8, od8;      // 8-bit counters: byte j = class 2j / class 2j+1
+    uint32_t pending;       // trips since the last warp flush (<= 255)
     uint64_t dy012, dy102;  // dyadic triads of classes 012 / 102
 };
+
+__device__ __forceinline__ void acc_init(Acc &c) {
+    c.n4 = c.ev8 = c.od8 = 0;
+    c.pending = 0;
+    c.dy012 = c.dy102 = 0;
+}
 
 __device__ __forceinline__ void add_dyadic(Acc &c, uint32_t pre, uint64_t x) {
     if (pre == 3u) c.dy102 += x;
     else c.dy012 += x;
 }
 
-__device__ __forceinline__ void acc_init(Acc &c) {
-    c.lo = c.hi = 0;
-    c.pending = 0;
-    c.dy012 = c.dy102 = 0;
+__device__ __forceinline__ void spill(Acc &c) {
+    c.ev8 += c.n4 & kNib;
+    c.od8 += (c.n4 >> 4) & kNib;
+    c.n4 = 0;
 }
 
-__device__ __forceinline__ void acc_flush(Acc &c, unsigned long long *sh) {
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Warp-level flush (all 32 lanes active): each connected class (3..15) is
+// summed over the warp with one REDUX and lane 0 adds it to the warp's own
+// shared slots (plain adds; 64-bit shared atomics are CAS loops on sm_100).
+__device__ __forceinline__ void warp_flush(Acc &c, unsigned long long *wsh) {
+    const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
-    for (int b = 0; b < 8; b++) {
-        uint32_t x = (uint32_t)(c.lo >> (8 * b)) & 255u;
-        if (x) atomicAdd(&sh[b], (unsigned long long)x);
+    for (int k = 3; k < 16; k++) {
+        uint32_t x = (uint32_t)(((k & 1) ? c.od8 : c.ev8) >> (8 * (k >> 1))) & 255u;
+        uint32_t s = __reduce_add_sync(0xffffffffu, x);
+        if (lane == 0) wsh[k] += s;
     }
-#pragma unroll
-    for (int b = 0; b < 8; b++) {
-        uint32_t x = (uint32_t)(c.hi >> (8 * b)) & 255u;
-        if (x) atomicAdd(&sh[8 + b], (unsigned long long)x);
-    }
-    c.lo = c.hi = 0;
+    c.ev8 = c.od8 = 0;
     c.pending = 0;
+}
+
+// flush before `len` more trips if any lane could overflow a byte counter
+__device__ __forceinline__ void warp_reserve(Acc &c, unsigned long long *wsh, uint32_t len) {
+    if (__any_sync(0xffffffffu, c.pending + len > 255u)) warp_flush(c, wsh);
+    c.pending += len;
 }
 
 // merge-path split of diagonal d: number of A elements among the first d
@@ -83,186 +115,190 @@ __device__ __forceinline__ uint32_t merge_path(const uint32_t *__restrict__ A, u
     return lo;
 }
 
-// classify the merged elements on diagonals [d0, d1) of dyad (u, v)
-__device__ __forceinline__ void merge_segment(const uint32_t *__restrict__ A, uint32_t a,
-                                              const uint32_t *__restrict__ B, uint32_t b,
-                                              uint32_t u, uint32_t v, uint32_t pre, uint32_t d0,
-                                              uint32_t d1, const uint8_t *__restrict__ tab,
-                                              Acc &c, unsigned long long *sh) {
-    uint32_t i = 0, j = 0;
-    if (d0 > 0) {
-        i = merge_path(A, a, B, b, d0);
-        j = d0 - i;
-        // the pair (A[i-1], B[j]) was consumed by the previous segment
-        if (i > 0 && j < b && (__ldg(A + i - 1) | 3u) == (__ldg(B + j) | 3u)) j++;
-    }
-    if (c.pending + (d1 - d0) > 255u) acc_flush(c, sh);
-    c.pending += d1 - d0;
+// Classify merge diagonals [d0, d1) of dyad (u, v).  A = adj[oa, oa+a),
+// B = adj[ob, ob+b), both followed by a sentinel; ku = u<<2|3, kv = v<<2|3;
+// tab = shared address of the 64-entry nibble-shift table.  The caller has
+// reserved d1 - d0 byte-counter increments (warp_reserve).
+__device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uint32_t oa,
+                                           uint32_t a, uint32_t ob, uint32_t b, uint32_t ku,
+                                           uint32_t kv, uint32_t pre, uint32_t d0, uint32_t d1,
+                                           uint32_t tab, Acc &c) {
+    uint32_t i = 0;
+    if (d0 > 0) i = merge_path(adj + oa, a, adj + ob, b, d0);
+    uint32_t pa = oa + i, pb = ob + (d0 - i);
+    uint32_t lastA = i > 0 ? (__ldg(adj + pa - 1) | 3u) : 0u;
+    // current heads and the next elements (sentinel-terminated rows)
+    uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
+    uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
     uint32_t I = 0;
-    while (i + j < d1) {
-        uint32_t x = i < a ? __ldg(A + i) : 0xffffffffu;
-        uint32_t y = j < b ? __ldg(B + j) : 0xffffffffu;
-        uint32_t kx = x | 3u, ky = y | 3u;
-        uint32_t ta = kx <= ky, tb = ky <= kx;
-        uint32_t w = (ta ? x : y) >> 2;
-        uint32_t tu = ta ? (x & 3u) : 0u;
-        uint32_t tv = tb ? (y & 3u) : 0u;
-        i += ta;
-        j += tb;
-        I += ta & tb;
-        uint32_t canon = (w > v) | ((tu == 0u) & (w > u));
-        uint32_t cls = tab[pre | (tu << 2) | (tv << 4)];
-        uint64_t inc = (uint64_t)canon << ((cls & 7u) * 8u);
-        if (cls & 8u) c.hi += inc;
-        else c.lo += inc;
+    const uint32_t tabp = tab + pre;
+    uint32_t t = d0;
+    while (t < d1) {
+        const uint32_t lim = min(d1, t + 15u);   // nibble counters hold 15
+        for (; t < lim; t++) {
+            const uint32_t kx = x | 3u, ky = y | 3u;
+            const bool ta = kx <= ky;            // consume A (ties: A first)
+            const bool tb = ky <= kx;            // B's id is the merged id
+            // code - pre = tu<<2 | tv<<4 with tu = tag in A, tv = tag in B
+            const uint32_t ca = ta ? ((x << 2) & 12u) : 0u;
+            const uint32_t cb = tb ? ((y << 4) & 48u) : 0u;
+            // A element: w > v.  B-only element: w > u, and not the B twin of
+            // the A element just consumed (already classified with both tags).
+            const bool canon = ta ? (kx > kv) : ((ky != lastA) & (ky > ku));
+            I += (uint32_t)(ta & tb);
+            const uint32_t sh = canon ? lds_u8(tabp + (ca | cb)) : 0u;
+            c.n4 += 1ull << sh;
+            lastA = ta ? kx : lastA;
+            pa += ta;
+            pb += !ta;
+            const uint32_t nv = __ldg(adj + (ta ? pa : pb) + 1u);
+            x = ta ? xn : x;
+            xn = ta ? nv : xn;
+            y = ta ? y : yn;
+            yn = ta ? yn : nv;
+        }
+        spill(c);
     }
     add_dyadic(c, pre, I);
 }
 
-__device__ __forceinline__ void block_setup(uint8_t *tab, unsigned long long *sh) {
-    if (threadIdx.x < 64) tab[threadIdx.x] = c_triad_table[threadIdx.x];
-    if (threadIdx.x < 16) sh[threadIdx.x] = 0;
+// shared table: code -> 4 * class (nibble shift); wsh[warp][16]: per-warp totals
+__device__ __forceinline__ void block_setup(uint8_t *tab, unsigned long long (*wsh)[16]) {
+    if (threadIdx.x < 64) tab[threadIdx.x] = (uint8_t)(4u * c_triad_table[threadIdx.x]);
+    for (int i = threadIdx.x; i < kWarps * 16; i += blockDim.x) (&wsh[0][0])[i] = 0;
     __syncthreads();
 }
 
-__device__ __forceinline__ void block_finish(Acc &c, unsigned long long *sh,
+__device__ __forceinline__ void block_finish(Acc &c, unsigned long long (*wsh)[16],
                                              unsigned long long *d_counts) {
-    acc_flush(c, sh);
-    // dyadic terms: warp reduce then shared atomics
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    warp_flush(c, wsh[warp]);
     unsigned long long d0 = c.dy012, d1 = c.dy102;
+#pragma unroll
     for (int o = 16; o; o >>= 1) {
         d0 += __shfl_xor_sync(0xffffffffu, d0, o);
         d1 += __shfl_xor_sync(0xffffffffu, d1, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sh[1], d0);
-        atomicAdd(&sh[2], d1);
+    if (lane == 0) {
+        wsh[warp][1] += d0;
+        wsh[warp][2] += d1;
     }
     __syncthreads();
-    if (threadIdx.x >= 1 && threadIdx.x < 16 && sh[threadIdx.x])
-        atomicAdd(&d_counts[threadIdx.x], sh[threadIdx.x]);
+    if (threadIdx.x >= 1 && threadIdx.x < 16) {
+        unsigned long long s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; w++) s += wsh[w][threadIdx.x];
+        if (s) atomicAdd(&d_counts[threadIdx.x], s);
+    }
 }
 
-__global__ void __launch_bounds__(256)
-k_census_thread(const BinItem2 *__restrict__ items, uint64_t count,
-                const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
-                unsigned long long *d_counts) {
-    __shared__ uint8_t tab[64];
-    __shared__ unsigned long long sh[16];
-    block_setup(tab, sh);
+// prefetch the 128-byte lines of adj[o, o+len] into L2 (fire and forget)
+__device__ __forceinline__ void prefetch_row_l2(const uint32_t *adj, uint32_t o, uint32_t len) {
+    const char *p = reinterpret_cast<const char *>(adj + o);
+    const char *e = reinterpret_cast<const char *>(adj + o + len);
+    for (const char *q = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)127);
+         q <= e; q += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
+}
+
+// row u of the sentinel-padded CSR: start and |N(u)|
+__device__ __forceinline__ void row_of(const uint32_t *__restrict__ off, uint32_t u,
+                                       uint32_t &o, uint32_t &len) {
+    o = __ldg(off + u);
+    len = __ldg(off + u + 1) - o - 1u;
+}
+
+// thread bin: one thread per dyad.  Block-persistent over tiles of
+// kPlanTile consecutive canonical dyads; inside a tile the plan ordered the
+// thread-bin dyads by cost, so each warp's lanes run equal trip counts while
+// the tile keeps the N(u) rows of nearby u hot in L1/L2.
+__global__ void __launch_bounds__(kCensusThreads)
+k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__ tile_count,
+                uint64_t ntiles, const uint32_t *__restrict__ off,
+                const uint32_t *__restrict__ adj, uint64_t n, unsigned long long *d_counts) {
+    __shared__ uint8_t tab_s[64];
+    __shared__ unsigned long long wsh[kWarps][16];
+    block_setup(tab_s, wsh);
+    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
-    for (uint64_t it = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; it < count;
-         it += (uint64_t)gridDim.x * blockDim.x) {
-        BinItem2 e = items[it];
-        uint32_t ev = __ldg(adj + e.p);
-        uint32_t v = ev >> 2, pre = ev & 3u;
-        uint32_t ou = __ldg(off + e.u), a = __ldg(off + e.u + 1) - ou;
-        uint32_t ov = __ldg(off + v), b = __ldg(off + v + 1) - ov;
-        add_dyadic(c, pre, n - a - b);
-        merge_segment(adj + ou, a, adj + ov, b, e.u, v, pre, 0, a + b, tab, c, sh);
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t cnt = __ldg(tile_count + tile);
+        const BinItem2 *it = items + tile * kPlanTile;
+        for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
+            const bool valid = base + lane < cnt;
+            BinItem2 e{0, 0};
+            uint32_t ou = 0, a = 0, ov = 0, b = 0;
+            if (valid) {
+                e = it[base + lane];
+                row_of(off, e.u, ou, a);
+                row_of(off, e.e >> 2, ov, b);
+                prefetch_row_l2(adj, ou, a);
+                prefetch_row_l2(adj, ov, b);
+            }
+            warp_reserve(c, wsh[warp], a + b);
+            if (valid) {
+                const uint32_t pre = e.e & 3u;
+                add_dyadic(c, pre, n - a - b);
+                merge_diag(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, 0, a + b, tab, c);
+            }
+        }
     }
-    block_finish(c, sh, d_counts);
+    block_finish(c, wsh, d_counts);
 }
 
-__global__ void __launch_bounds__(256)
-k_census_warp(const BinItem2 *__restrict__ items, uint64_t count,
+// warp bin: one warp per item = one dyad's diagonals [d0, d1), 32 lane
+// segments of <= kLaneSpan diagonals each
+__global__ void __launch_bounds__(kCensusThreads)
+k_census_warp(const BinItem4 *__restrict__ items, const unsigned long long *__restrict__ d_count,
               const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
               unsigned long long *d_counts) {
-    __shared__ uint8_t tab[64];
-    __shared__ unsigned long long sh[16];
-    block_setup(tab, sh);
+    __shared__ uint8_t tab_s[64];
+    __shared__ unsigned long long wsh[kWarps][16];
+    block_setup(tab_s, wsh);
+    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
-    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t count = *d_count;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t it = wid; it < count; it += nw) {
-        BinItem2 e = items[it];
-        uint32_t ev = __ldg(adj + e.p);
-        uint32_t v = ev >> 2, pre = ev & 3u;
-        uint32_t ou = __ldg(off + e.u), a = __ldg(off + e.u + 1) - ou;
-        uint32_t ov = __ldg(off + v), b = __ldg(off + v + 1) - ov;
-        uint32_t cst = a + b, per = (cst + 31) >> 5;
-        uint32_t d0 = lane * per, d1 = min(cst, d0 + per);
-        if (lane == 0) add_dyadic(c, pre, n - a - b);
-        if (d0 < d1) merge_segment(adj + ou, a, adj + ov, b, e.u, v, pre, d0, d1, tab, c, sh);
+        const BinItem4 e = items[it];
+        const uint32_t v = e.e >> 2, pre = e.e & 3u;
+        uint32_t ou, a, ov, b;
+        row_of(off, e.u, ou, a);
+        row_of(off, v, ov, b);
+        const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
+        const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
+        warp_reserve(c, wsh[warp], d1 - d0);
+        if (e.d0 == 0 && lane == 0) add_dyadic(c, pre, n - a - b);
+        if (d0 < d1)
+            merge_diag(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, d0, d1, tab, c);
     }
-    block_finish(c, sh, d_counts);
-}
-
-__global__ void __launch_bounds__(kBlockThreads)
-k_census_block(const BinItem4 *__restrict__ items, uint64_t count,
-               const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
-               unsigned long long *d_counts) {
-    __shared__ uint8_t tab[64];
-    __shared__ unsigned long long sh[16];
-    block_setup(tab, sh);
-    Acc c;
-    acc_init(c);
-    for (uint64_t it = blockIdx.x; it < count; it += gridDim.x) {
-        BinItem4 e = items[it];
-        uint32_t ev = __ldg(adj + e.p);
-        uint32_t v = ev >> 2, pre = ev & 3u;
-        uint32_t ou = __ldg(off + e.u), a = __ldg(off + e.u + 1) - ou;
-        uint32_t ov = __ldg(off + v), b = __ldg(off + v + 1) - ov;
-        uint32_t span = e.d1 - e.d0, per = (span + kBlockThreads - 1) / kBlockThreads;
-        uint32_t d0 = e.d0 + threadIdx.x * per, d1 = min(e.d1, d0 + per);
-        if (e.d0 == 0 && threadIdx.x == 0) add_dyadic(c, pre, n - a - b);
-        if (d0 < d1) merge_segment(adj + ou, a, adj + ov, b, e.u, v, pre, d0, d1, tab, c, sh);
-    }
-    block_finish(c, sh, d_counts);
-}
-
-inline unsigned grid_cap(uint64_t blocks, unsigned cap) {
-    if (blocks < 1) blocks = 1;
-    return (unsigned)(blocks < cap ? blocks : cap);
+    block_finish(c, wsh, d_counts);
 }
 
 }  // namespace
 
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
-                      tc_profile *prof, uint64_t *launches) {
+                      cudaEvent_t *ev, uint64_t *launches) {
     const uint64_t n = g->st.n;
     unsigned long long *out = reinterpret_cast<unsigned long long *>(d_counts);
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    if (prof) {
-        for (int i = 0; i < 4; i++) TC_CUDA(cudaEventCreate(&ev[i]));
-        TC_CUDA(cudaEventRecord(ev[0], s));
-    }
-    const unsigned sms = 148;
-    if (bl.count[0]) {
-        k_census_thread<<<grid_cap((bl.count[0] + 255) / 256, sms * 8), 256, 0, s>>>(
-            bl.t, bl.count[0], g->off, g->adj, n, out);
-        TC_CUDA(cudaGetLastError());
-        *launches += 1;
-    }
-    if (prof) TC_CUDA(cudaEventRecord(ev[1], s));
-    if (bl.count[1]) {
-        k_census_warp<<<grid_cap((bl.count[1] + 7) / 8, sms * 8), 256, 0, s>>>(
-            bl.w, bl.count[1], g->off, g->adj, n, out);
-        TC_CUDA(cudaGetLastError());
-        *launches += 1;
-    }
-    if (prof) TC_CUDA(cudaEventRecord(ev[2], s));
-    if (bl.count[2]) {
-        k_census_block<<<grid_cap(bl.count[2], sms * 8), kBlockThreads, 0, s>>>(
-            bl.b, bl.count[2], g->off, g->adj, n, out);
-        TC_CUDA(cudaGetLastError());
-        *launches += 1;
-    }
-    if (prof) {
-        TC_CUDA(cudaEventRecord(ev[3], s));
-        TC_CUDA(cudaEventSynchronize(ev[3]));
-        float t;
-        for (int i = 0; i < 3; i++) {
-            TC_CUDA(cudaEventElapsedTime(&t, ev[i], ev[i + 1]));
-            prof->kernel_ms[i] = t;
-        }
-        TC_CUDA(cudaEventElapsedTime(&t, ev[0], ev[3]));
-        prof->census_ms = t;
-        for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
-    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    const unsigned grid = (unsigned)sms * kCensusBlocksPerSM;
+    const size_t dyn = 0;
+    if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
+    k_census_thread<<<grid, kCensusThreads, dyn, s>>>(bl.t, bl.t_count, bl.ntiles, g->off, g->adj,
+                                                     n, out);
+    TC_CUDA(cudaGetLastError());
+    if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
+    k_census_warp<<<grid, kCensusThreads, 0, s>>>(bl.w, bl.w_count, g->off, g->adj, n, out);
+    TC_CUDA(cudaGetLastError());
+    if (ev) TC_CUDA(cudaEventRecord(ev[2], s));
+    *launches += 2;
     return TC_OK;
 }
 

@@ -3,16 +3,25 @@
 
 namespace tc {
 
-// Work lists of the degree-binned scheduler (a2), device pointers.
+// Work lists of the degree-binned scheduler (a2), all device memory.  The
+// item counts stay on the device (the kernels read them), so planning and
+// the census need no host round trip.
 struct BinLists {
-    const BinItem2 *t = nullptr;   // thread bin: one thread per dyad
-    const BinItem2 *w = nullptr;   // warp bin: one warp per dyad
-    const BinItem4 *b = nullptr;   // block bin: one block per <= kBlockSpan diagonals
-    uint64_t count[kNumBins] = {0, 0, 0};
+    const BinItem2 *t = nullptr;            // thread bin: tile-local lists sorted by cost
+    const uint32_t *t_count = nullptr;      // device: thread-bin items per tile
+    uint64_t ntiles = 0;                    // tiles of kPlanTile canonical dyads
+    const BinItem4 *w = nullptr;            // warp bin: <= kWarpChunk diagonals per item
+    const unsigned long long *w_count = nullptr;   // device: number of warp-bin items
 };
+
+constexpr int kCensusThreads = 256;
+constexpr int kPlanThreads = 256;
+constexpr int kPlanItems = 16;
+constexpr int kPlanTile = kPlanThreads * kPlanItems;   // canonical dyads per plan tile
+constexpr unsigned kCensusBlocksPerSM = 8;
 
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
-                      tc_profile *prof, uint64_t *launches);
+                      cudaEvent_t *ev /* 3 events or null */, uint64_t *launches);
 
 }  // namespace tc

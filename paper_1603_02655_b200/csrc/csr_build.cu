@@ -9,13 +9,17 @@
 //                (d<<32 | s<<2 | 2); self-loops -> all-ones sentinel keys
 //                that sort last (strict digraph); range check.
 //   2. sort      LSD radix sort on the column bits then the row bits.
-//   3. scan      head = first key of a (row, col) run; one fused exclusive
-//                scan counts heads (entry index r) and canonical heads
-//                row < col (dyad index k, canonical order P:277-281) and its
-//                output pass ORs the run's tags (dedup, mutual merge),
-//                writes adj[r] = col<<2 | tag, the dyad list, and the row
-//                offsets at row boundaries.
-//   4. stats     m, mutual dyads, sum d^2, max degree.
+//   3. compact   head = first key of a (row, col) run.  A ballot/popc
+//                compaction (count pass, scan of tile counts, write pass)
+//                numbers the heads (entry index r) and the canonical heads
+//                row < col (dyad index k, canonical order P:277-281); each
+//                head ORs its run's tags (dedup, mutual merge) and writes
+//                adj[r + row] = col<<2 | tag, the dyad list and, at row
+//                boundaries, the row offsets.  Every row ends with one
+//                sentinel entry 0xffffffff (greater than any real entry), so
+//                the census merge runs off a row end without bounds checks:
+//                row u = adj[off[u], off[u+1] - 1), |N(u)| = off[u+1]-off[u]-1.
+//   4. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost.
 #include <stdio.h>
 
 #include "radix_sort.cuh"
@@ -26,6 +30,10 @@ namespace tc {
 namespace {
 
 constexpr uint64_t kSentinel = ~0ull;
+constexpr int kHcThreads = 256;
+constexpr int kHcWarps = kHcThreads / 32;
+constexpr int kHcItems = 16;
+constexpr int kHcTile = kHcThreads * kHcItems;   // keys per block
 
 __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                        uint64_t m, uint64_t n, uint64_t *__restrict__ keys,
@@ -34,72 +42,135 @@ __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restr
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = src[i], d = dst[i];
+        ulonglong2 kv;
         if (s >= n || d >= n) {
             atomicMin(&scratch[0], (unsigned long long)i);
-            keys[2 * i] = kSentinel;
-            keys[2 * i + 1] = kSentinel;
-            continue;
-        }
-        if (s == d) {
+            kv = make_ulonglong2(kSentinel, kSentinel);
+        } else if (s == d) {
             loops++;
-            keys[2 * i] = kSentinel;
-            keys[2 * i + 1] = kSentinel;
+            kv = make_ulonglong2(kSentinel, kSentinel);
         } else {
-            keys[2 * i] = ((uint64_t)s << 32) | ((uint64_t)d << 2) | 1ull;
-            keys[2 * i + 1] = ((uint64_t)d << 32) | ((uint64_t)s << 2) | 2ull;
+            kv = make_ulonglong2(((uint64_t)s << 32) | ((uint64_t)d << 2) | 1ull,
+                                 ((uint64_t)d << 32) | ((uint64_t)s << 2) | 2ull);
         }
+        reinterpret_cast<ulonglong2 *>(keys)[i] = kv;
     }
-    // warp-aggregated loop count
     for (int o = 16; o; o >>= 1) loops += __shfl_xor_sync(0xffffffffu, loops, o);
     if ((threadIdx.x & 31) == 0 && loops) atomicAdd(&scratch[1], loops);
 }
 
-struct HeadIn {
-    const uint64_t *key;
-    __device__ __forceinline__ uint64_t operator()(size_t i) const {
-        uint64_t k = key[i];
-        bool head = (i == 0) || ((key[i - 1] >> 2) != (k >> 2));
-        bool canon = head && ((uint32_t)(k >> 32) < (uint32_t)((k >> 2) & 0x3fffffffu));
-        return (uint64_t)head | ((uint64_t)canon << 32);
-    }
-};
+// (row, col) of a sorted key; heads: first key of each (row, col) run
+__device__ __forceinline__ uint32_t key_row(uint64_t k) { return (uint32_t)(k >> 32); }
+__device__ __forceinline__ uint32_t key_col(uint64_t k) { return (uint32_t)((k >> 2) & 0x3fffffffu); }
 
-struct HeadOut {
-    const uint64_t *key;
-    size_t L;
-    uint32_t *adj, *du, *dp, *off;
-    __device__ __forceinline__ void operator()(size_t i, uint64_t excl, uint64_t v) const {
-        if (!(v & 1ull)) return;
-        uint32_t r = (uint32_t)excl, k = (uint32_t)(excl >> 32);
-        uint64_t kk = key[i];
-        uint32_t row = (uint32_t)(kk >> 32);
-        uint32_t col = (uint32_t)((kk >> 2) & 0x3fffffffu);
-        uint32_t tag = (uint32_t)(kk & 3u);
-        for (size_t j = i + 1; j < L && (key[j] >> 2) == (kk >> 2); j++) tag |= (uint32_t)(key[j] & 3u);
-        adj[r] = (col << 2) | tag;
-        if (v >> 32) {
-            du[k] = row;
-            dp[k] = r;
-        }
-        // first entry of row `row`: rows (prev_row, row] start at r
-        uint32_t first = 0;
-        bool boundary = (i == 0);
-        if (!boundary) {
-            uint32_t prev = (uint32_t)(key[i - 1] >> 32);
-            if (prev != row) {
-                boundary = true;
-                first = prev + 1;
+// flags of key i (warp-striped: lanes hold consecutive keys)
+__device__ __forceinline__ void head_flags(const uint64_t *__restrict__ key, size_t L, size_t i,
+                                           uint64_t &k, uint64_t &prev, bool &head, bool &canon) {
+    const uint32_t lane = threadIdx.x & 31;
+    k = i < L ? __ldg(key + i) : kSentinel;
+    prev = __shfl_up_sync(0xffffffffu, k, 1);
+    if (lane == 0) prev = (i > 0 && i - 1 < L) ? __ldg(key + i - 1) : kSentinel;
+    head = i < L && (i == 0 || (prev >> 2) != (k >> 2));
+    canon = head && key_row(k) < key_col(k);
+}
+
+// pass 1: per tile, number of heads | canonical heads << 32
+__global__ void __launch_bounds__(kHcThreads)
+k_head_count(const uint64_t *__restrict__ key, size_t L, uint64_t *__restrict__ tile_tot) {
+    __shared__ uint64_t wsum[kHcWarps];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
+    uint32_t nh = 0, nc = 0;
+#pragma unroll 4
+    for (int r = 0; r < kHcItems; r++) {
+        uint64_t k, prev;
+        bool head, canon;
+        head_flags(key, L, base + (size_t)r * 32 + lane, k, prev, head, canon);
+        nh += __popc(__ballot_sync(0xffffffffu, head));
+        nc += __popc(__ballot_sync(0xffffffffu, canon));
+    }
+    if (lane == 0) wsum[warp] = (uint64_t)nh | ((uint64_t)nc << 32);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int w = 0; w < kHcWarps; w++) t += wsum[w];
+        tile_tot[blockIdx.x] = t;
+    }
+}
+
+// pass 2: write adj / dyad lists / row offsets at the compacted positions
+__global__ void __launch_bounds__(kHcThreads)
+k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restrict__ tile_off,
+             uint32_t *__restrict__ adj, uint32_t *__restrict__ du, uint32_t *__restrict__ de,
+             uint32_t *__restrict__ off) {
+    __shared__ uint64_t wsum[kHcWarps];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
+    // warp totals (L1-hot re-read of the warp's 512 keys) -> warp offsets
+    uint32_t nh = 0, nc = 0;
+#pragma unroll 4
+    for (int r = 0; r < kHcItems; r++) {
+        uint64_t k, prev;
+        bool head, canon;
+        head_flags(key, L, base + (size_t)r * 32 + lane, k, prev, head, canon);
+        nh += __popc(__ballot_sync(0xffffffffu, head));
+        nc += __popc(__ballot_sync(0xffffffffu, canon));
+    }
+    if (lane == 0) wsum[warp] = (uint64_t)nh | ((uint64_t)nc << 32);
+    __syncthreads();
+    uint64_t woff = tile_off[blockIdx.x];
+    for (uint32_t w = 0; w < warp; w++) woff += wsum[w];
+    uint32_t r0 = (uint32_t)woff, k0 = (uint32_t)(woff >> 32);
+    for (int r = 0; r < kHcItems; r++) {
+        const size_t i = base + (size_t)r * 32 + lane;
+        uint64_t k, prev;
+        bool head, canon;
+        head_flags(key, L, i, k, prev, head, canon);
+        const uint32_t bh = __ballot_sync(0xffffffffu, head);
+        const uint32_t bc = __ballot_sync(0xffffffffu, canon);
+        if (head) {
+            const uint32_t rr = r0 + __popc(bh & lt);
+            const uint32_t row = key_row(k), col = key_col(k);
+            uint32_t tag = (uint32_t)(k & 3u);
+            for (size_t j = i + 1; j < L; j++) {       // OR the run's tags
+                uint64_t kj = __ldg(key + j);
+                if ((kj >> 2) != (k >> 2)) break;
+                tag |= (uint32_t)(kj & 3u);
             }
+            const uint32_t e = (col << 2) | tag;
+            adj[rr + row] = e;
+            if (canon) {
+                const uint32_t kk = k0 + __popc(bc & lt);
+                du[kk] = row;
+                de[kk] = e;
+            }
+            // first entry of row `row`: rows (prev_row, row] start here
+            uint32_t first = 0;
+            bool boundary = (i == 0);
+            if (!boundary && key_row(prev) != row) {
+                boundary = true;
+                first = key_row(prev) + 1;
+            }
+            if (boundary)
+                for (uint32_t x = first; x <= row; x++) off[x] = rr + x;
         }
-        if (boundary)
-            for (uint32_t x = first; x <= row; x++) off[x] = r;
+        r0 += __popc(bh);
+        k0 += __popc(bc);
     }
-};
+}
 
-__global__ void k_fill_tail(uint32_t *off, uint64_t from, uint64_t n, uint32_t val) {
+__global__ void k_fill_tail(uint32_t *off, uint64_t from, uint64_t n, uint32_t nnz) {
     for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
          x += (uint64_t)gridDim.x * blockDim.x)
-        off[x] = val;
+        off[x] = nnz + (uint32_t)x;
+}
+
+// row terminators (and slack entries past the last row for look-ahead loads)
+__global__ void k_sentinels(const uint32_t *__restrict__ off, uint64_t n, uint32_t *adj) {
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n + 8;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        adj[x < n ? off[x + 1] - 1 : off[n] + (x - n)] = 0xffffffffu;
 }
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
@@ -113,7 +184,7 @@ __global__ void k_vertex_stats(const uint32_t *__restrict__ off, uint64_t n,
     unsigned long long s2 = 0, mx = 0;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (uint64_t)gridDim.x * blockDim.x) {
-        unsigned long long d = off[u + 1] - off[u];
+        unsigned long long d = off[u + 1] - off[u] - 1;
         s2 += d * d;
         mx = d > mx ? d : mx;
     }
@@ -128,13 +199,17 @@ __global__ void k_vertex_stats(const uint32_t *__restrict__ off, uint64_t n,
     }
 }
 
-// [2] = distinct arcs m, [3] = mutual dyads
-__global__ void k_dyad_stats(const uint32_t *__restrict__ adj, const uint32_t *__restrict__ dp,
-                             uint64_t D, unsigned long long *out) {
+// per canonical dyad: cost c = |N(u)| + |N(v)| (uniform workload);
+// stats [2] = distinct arcs m, [3] = mutual dyads
+__global__ void k_dyad_cost_stats(const uint32_t *__restrict__ off,
+                                  const uint32_t *__restrict__ du,
+                                  const uint32_t *__restrict__ de, uint64_t D,
+                                  uint32_t *__restrict__ dc, unsigned long long *out) {
     unsigned long long m = 0, mu = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < D;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t t = adj[dp[k]] & 3u;
+        uint32_t u = du[k], e = de[k], v = e >> 2, t = e & 3u;
+        dc[k] = (__ldg(off + u + 1) - __ldg(off + u)) + (__ldg(off + v + 1) - __ldg(off + v)) - 2;
         m += __popc(t);
         mu += (t == 3u);
     }
@@ -185,6 +260,11 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     }
     const uint64_t loops = h[1];
     const size_t L = L0 - 2 * loops;
+    if ((uint64_t)L + n + 8 >= (1ull << 32)) {
+        set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
+                  (unsigned long long)(L + n));
+        return TC_E_INVALID;
+    }
 
     // 2. sort by (row, col): column bits first, then row bits
     int b = 1;
@@ -197,39 +277,51 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         TC_OK)
         return st;
 
-    // 3. fused head scan -> adj, dyad list, offsets
+    // 3. compaction -> adj, dyad list, offsets
     size_t cap = L ? L : 1;
-    uint32_t *adj = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
+    uint32_t *adj = (uint32_t *)mem.alloc((L + n + 8) * sizeof(uint32_t));
     uint32_t *du = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
-    uint32_t *dp = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
+    uint32_t *de = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
+    uint32_t *dc = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
     uint32_t *off = (uint32_t *)mem.alloc((n + 1) * sizeof(uint32_t));
-    g->adj = adj; g->adj_n = cap;
+    g->adj = adj; g->adj_n = L + n + 8;
     g->dyad_u = du; g->dyad_n = cap / 2 + 1;
-    g->dyad_p = dp;
+    g->dyad_e = de;
+    g->dyad_c = dc;
     g->off = off; g->off_n = n + 1;
-    if (!adj || !du || !dp || !off) {
+    if (!adj || !du || !de || !dc || !off) {
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
-    DevBuf<uint64_t> total;
-    if ((st = total.allocate(mem, 1)) != TC_OK) return st;
-    st = scan_exclusive<uint64_t>(mem, L, HeadIn{sorted}, HeadOut{sorted, L, adj, du, dp, off},
-                                  total.p, s, &g->launches);
-    if (st != TC_OK) return st;
     uint64_t tot = 0, lastkey = 0;
-    TC_CUDA(cudaMemcpyAsync(&tot, total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
-    if (L) TC_CUDA(cudaMemcpyAsync(&lastkey, sorted + (L - 1), sizeof(uint64_t),
-                                   cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
+    if (L) {
+        const size_t ntiles = (L + kHcTile - 1) / kHcTile;
+        DevBuf<uint64_t> tt, total;
+        if ((st = tt.allocate(mem, ntiles)) != TC_OK) return st;
+        if ((st = total.allocate(mem, 1)) != TC_OK) return st;
+        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p);
+        TC_CUDA(cudaGetLastError());
+        st = scan_exclusive<uint64_t>(mem, ntiles, ArrayIn<uint64_t>{tt.p},
+                                      ArrayOutExcl<uint64_t>{tt.p}, total.p, s, &g->launches);
+        if (st != TC_OK) return st;
+        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p, adj, du, de, off);
+        TC_CUDA(cudaGetLastError());
+        g->launches += 2;
+        TC_CUDA(cudaMemcpyAsync(&tot, total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaMemcpyAsync(&lastkey, sorted + (L - 1), sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+    }
     const uint64_t nnz = tot & 0xffffffffull, D = tot >> 32;
     uint64_t from = L ? ((lastkey >> 32) + 1) : 0;
     k_fill_tail<<<grid_for(n + 1 - from, 256), 256, 0, s>>>(off, from, n, (uint32_t)nnz);
-    g->launches++;
+    k_sentinels<<<grid_for(n + 8, 256), 256, 0, s>>>(off, n, adj);
+    g->launches += 2;
     TC_CUDA(cudaGetLastError());
 
     // 4. stats
     k_vertex_stats<<<grid_for(n, 256), 256, 0, s>>>(off, n, scratch.p + 4);
-    if (D) k_dyad_stats<<<grid_for(D, 256), 256, 0, s>>>(adj, dp, D, scratch.p + 4);
+    if (D) k_dyad_cost_stats<<<grid_for(D, 256), 256, 0, s>>>(off, du, de, D, dc, scratch.p + 4);
     g->launches += D ? 2 : 1;
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -1,13 +1,15 @@
 // radix_sort.cu -- hand-written LSD radix sort of 64-bit keys on selected bit
 // fields (a1's sort; SURVEY.md section 7 decision D1: written here, no CUB).
 //
-// One pass per digit of <= 8 bits:
-//   upsweep    per-tile digit histogram (per-warp shared counters)
-//   scan       exclusive scan of the digit-major histogram (scan.cuh)
-//   downsweep  stable scatter: per warp, __match_any_sync groups the lanes
-//              holding the same digit, rank = earlier peers + running per-warp
-//              digit count; warp offsets within the tile come from a scan over
-//              warps in shared memory.
+// One pass per digit of <= 8 bits (256 buckets), tiles of 4096 keys:
+//   upsweep    per-tile digit histogram (shared-memory atomics)
+//   scan       exclusive scan of the digit-major (digit, tile) histogram
+//   downsweep  stable tile-local counting sort: per warp, __match_any_sync
+//              groups the lanes holding the same digit (rank = earlier peers
+//              + running per-warp digit count, 16-bit shared counters); the
+//              tile is reordered by digit in shared memory and written out
+//              so consecutive threads store consecutive addresses of each
+//              digit run (coalesced), instead of a 32-way scatter per warp.
 #include "radix_sort.cuh"
 #include "scan.cuh"
 
@@ -19,77 +21,96 @@ constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
 constexpr int kRsItems = 16;
 constexpr int kRsTile = kRsThreads * kRsItems;   // 4096 keys per block
-constexpr int kMaxRadix = 256;
+constexpr int kMaxBits = 8;
+constexpr int kMaxRadix = 1 << kMaxBits;
 
 __global__ void __launch_bounds__(kRsThreads)
 rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask, int radix,
            uint32_t *__restrict__ hist, size_t ntiles) {
-    __shared__ uint32_t wh[kRsWarps][kMaxRadix];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kRsWarps * kMaxRadix; i += kRsThreads) (&wh[0][0])[i] = 0;
+    __shared__ uint32_t h[kMaxRadix];
+    for (int i = threadIdx.x; i < radix; i += kRsThreads) h[i] = 0;
     __syncthreads();
-    size_t base = (size_t)blockIdx.x * kRsTile + (size_t)warp * 32 * kRsItems;
+    const size_t base = (size_t)blockIdx.x * kRsTile;
 #pragma unroll 4
     for (int k = 0; k < kRsItems; k++) {
-        size_t i = base + (size_t)k * 32 + lane;
-        if (i < n) {
-            uint32_t d = (uint32_t)(keys[i] >> shift) & mask;
-            atomicAdd(&wh[warp][d], 1u);
-        }
+        size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
+        if (i < n) atomicAdd(&h[(uint32_t)(__ldg(keys + i) >> shift) & mask], 1u);
     }
     __syncthreads();
-    for (int d = threadIdx.x; d < radix; d += kRsThreads) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int w = 0; w < kRsWarps; w++) s += wh[w][d];
-        hist[(size_t)d * ntiles + blockIdx.x] = s;
-    }
+    for (int d = threadIdx.x; d < radix; d += kRsThreads) hist[(size_t)d * ntiles + blockIdx.x] = h[d];
 }
 
-__global__ void __launch_bounds__(kRsThreads)
+struct DownSmem {
+    uint32_t klo[kRsTile], khi[kRsTile];     // tile reordered by digit (split halves:
+                                             // 4-byte banks, fewer store conflicts)
+    uint16_t wc[kRsWarps][kMaxRadix];        // per-warp digit counts, then offsets
+    uint32_t gbase[kMaxRadix];               // global offset - local offset per digit
+};
+
+__global__ void __launch_bounds__(kRsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
              uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles) {
-    __shared__ uint32_t wc[kRsWarps][kMaxRadix];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    DownSmem &S = *reinterpret_cast<DownSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int i = threadIdx.x; i < kRsWarps * kMaxRadix; i += kRsThreads) (&wc[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < kRsWarps * radix; i += kRsThreads) S.wc[i / radix][i % radix] = 0;
     __syncthreads();
     const uint32_t lt = (1u << lane) - 1u;
-    size_t base = (size_t)blockIdx.x * kRsTile + (size_t)warp * 32 * kRsItems;
+    const size_t tile0 = (size_t)blockIdx.x * kRsTile;
+    const size_t wbase = tile0 + (size_t)warp * 32 * kRsItems;
     uint64_t key[kRsItems];
     uint32_t rank[kRsItems];
 #pragma unroll
     for (int k = 0; k < kRsItems; k++) {
-        size_t i = base + (size_t)k * 32 + lane;
+        size_t i = wbase + (size_t)k * 32 + lane;
         bool valid = i < n;
-        key[k] = valid ? keys[i] : 0ull;
+        key[k] = valid ? __ldg(keys + i) : 0ull;
         uint32_t d = valid ? ((uint32_t)(key[k] >> shift) & mask) : 0x10000u;
         uint32_t peers = __match_any_sync(0xffffffffu, d);
         uint32_t r = 0;
-        if (valid) r = wc[warp][d] + __popc(peers & lt);
+        if (valid) r = S.wc[warp][d] + __popc(peers & lt);
         __syncwarp();
-        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        if (valid && (peers & lt) == 0) S.wc[warp][d] += __popc(peers);
         __syncwarp();
         rank[k] = r;
     }
     __syncthreads();
-    // per digit: exclusive scan over warps + global offset of (digit, tile)
-    for (int d = threadIdx.x; d < radix; d += kRsThreads) {
-        uint32_t run = offs[(size_t)d * ntiles + blockIdx.x];
-#pragma unroll
-        for (int w = 0; w < kRsWarps; w++) {
-            uint32_t c = wc[w][d];
-            wc[w][d] = run;
-            run += c;
+    // tile-local digit offsets: exclusive scan over digits of the digit totals
+    // (each thread owns radix/256 consecutive digits), then per-warp offsets
+    {
+        const int per = (radix + kRsThreads - 1) / kRsThreads;
+        const int d0 = threadIdx.x * per;
+        uint32_t tot = 0;
+        for (int d = d0; d < d0 + per && d < radix; d++)
+            for (int w = 0; w < kRsWarps; w++) tot += S.wc[w][d];
+        uint32_t all;
+        uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
+        for (int d = d0; d < d0 + per && d < radix; d++) {
+            S.gbase[d] = offs[(size_t)d * ntiles + blockIdx.x] - run;
+            for (int w = 0; w < kRsWarps; w++) {
+                uint32_t c = S.wc[w][d];
+                S.wc[w][d] = (uint16_t)run;
+                run += c;
+            }
         }
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kRsItems; k++) {
-        size_t i = base + (size_t)k * 32 + lane;
+        size_t i = wbase + (size_t)k * 32 + lane;
         if (i < n) {
             uint32_t d = (uint32_t)(key[k] >> shift) & mask;
-            out[wc[warp][d] + rank[k]] = key[k];
+            const uint32_t pos = S.wc[warp][d] + rank[k];
+            S.klo[pos] = (uint32_t)key[k];
+            S.khi[pos] = (uint32_t)(key[k] >> 32);
         }
+    }
+    __syncthreads();
+    const uint32_t cnt = (uint32_t)min((size_t)kRsTile, n - tile0);
+    for (uint32_t i = threadIdx.x; i < cnt; i += kRsThreads) {
+        uint64_t k = ((uint64_t)S.khi[i] << 32) | S.klo[i];
+        uint32_t d = (uint32_t)(k >> shift) & mask;
+        out[S.gbase[d] + i] = k;
     }
 }
 
@@ -104,15 +125,19 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         set_error("radix sort: %zu keys exceed the 32-bit offset range", n);
         return TC_E_INVALID;
     }
+    TC_CUDA(cudaFuncSetAttribute(rs_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(DownSmem)));
     size_t ntiles = (n + kRsTile - 1) / kRsTile;
+    int maxbits = 1;
+    for (int p = 0; p < npasses; p++) maxbits = passes[p].bits > maxbits ? passes[p].bits : maxbits;
     DevBuf<uint32_t> hist;
-    tc_status st = hist.allocate(mem, ntiles * kMaxRadix);
+    tc_status st = hist.allocate(mem, ntiles << maxbits);
     if (st != TC_OK) return st;
     uint64_t *src = keys, *dst = tmp;
     for (int p = 0; p < npasses; p++) {
         int bits = passes[p].bits;
-        if (bits < 1 || bits > 8) {
-            set_error("radix sort: digit width %d out of [1,8]", bits);
+        if (bits < 1 || bits > kMaxBits) {
+            set_error("radix sort: digit width %d out of [1,%d]", bits, kMaxBits);
             return TC_E_INVALID;
         }
         int radix = 1 << bits;
@@ -124,8 +149,8 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
                                       ArrayOutExcl<uint32_t>{hist.p}, (uint32_t *)nullptr, s,
                                       launches);
         if (st != TC_OK) return st;
-        rs_downsweep<<<(unsigned)ntiles, kRsThreads, 0, s>>>(src, dst, n, passes[p].shift, mask,
-                                                             radix, hist.p, ntiles);
+        rs_downsweep<<<(unsigned)ntiles, kRsThreads, sizeof(DownSmem), s>>>(
+            src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles);
         TC_CUDA(cudaGetLastError());
         if (launches) *launches += 2;
         uint64_t *t = src;
@@ -136,12 +161,10 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
     return TC_OK;
 }
 
-}  // namespace tc
-
-namespace tc {
+// passes covering bits [lo, lo + width) with digits of at most 11 bits
 int radix_passes_for(int lo, int width, RadixPass *out) {
     if (width <= 0) return 0;
-    int np = (width + 7) / 8;
+    int np = (width + kMaxBits - 1) / kMaxBits;
     int per = (width + np - 1) / np;
     int done = 0, k = 0;
     while (done < width) {
@@ -153,4 +176,5 @@ int radix_passes_for(int lo, int width, RadixPass *out) {
     }
     return k;
 }
+
 }  // namespace tc

@@ -1,13 +1,18 @@
 // schedule.cu -- a2: degree-binned canonical-dyad scheduler + shard cuts.
 //
-// Each canonical dyad (u, v), u < v, gets the paper's uniform workload
+// Each canonical dyad (u, v), u < v, carries the paper's uniform workload
 // estimate c = |N(u)| + |N(v)| (Fig. P:1678-1705, "NsetSize + |N[u]| + |N[v]|
-// - 2"; the constant -2 does not change any bin or cut) and is
-// placed in one of three bins so power-law hubs do not serialise a warp:
-//   thread bin  c <= kThreadBinMax      one thread merges the whole dyad
-//   warp bin    c <= kWarpBinMax        32 lanes split it by merge-path
-//   block bin   c >  kWarpBinMax        chunks of kBlockSpan diagonals, one
-//                                       256-thread block per chunk
+// - 2"; the constant -2 changes no bin and no cut), computed
+// once by the CSR builder (dyad_c).  The plan is one stable counting sort of
+// the dyad range by c (256 digits: c itself for c <= kThreadBinMax, 255 for
+// every larger dyad):
+//   thread bin  c <= 254    items (u, e) ordered by c, so each warp holds
+//                           dyads of equal cost and its lanes run equal trip
+//                           counts (c merge diagonals each)
+//   warp bin    c > 254     the dyad is cut into warp items of <= 8160
+//                           diagonals (32 lanes x <= 255), so power-law hubs
+//                           spread over many warps and never serialise one
+// All counts stay on the device: no host synchronisation in the census.
 // The same costs, prefix-summed in canonical order, give the degree-balanced
 // multi-GPU shard cuts: the paper's uniform task
 // queues with one "queue" per GPU.
@@ -18,99 +23,105 @@ namespace tc {
 
 namespace {
 
-__device__ __forceinline__ uint32_t dyad_cost(const uint32_t *__restrict__ off,
-                                              const uint32_t *__restrict__ adj, uint32_t u,
-                                              uint32_t p, uint32_t *v_out) {
-    uint32_t v = __ldg(adj + p) >> 2;
-    *v_out = v;
-    return (__ldg(off + u + 1) - __ldg(off + u)) + (__ldg(off + v + 1) - __ldg(off + v));
+constexpr int kPlanWarps = kPlanThreads / 32;
+constexpr int kDigits = 256;
+
+__device__ __forceinline__ uint32_t digit_of(uint32_t c) {
+    return c <= kThreadBinMax ? c : 255u;
 }
 
-__device__ __forceinline__ int bin_of(uint32_t c) {
-    return c <= kThreadBinMax ? 0 : (c <= kWarpBinMax ? 1 : 2);
-}
-
-// cnt[0..2] items per bin (bin 2 counts chunks), cnt[3..5] work per bin
-__global__ void k_plan_count(const uint32_t *__restrict__ du, const uint32_t *__restrict__ dp,
-                             const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj,
-                             uint64_t k0, uint64_t k1, unsigned long long *cnt) {
-    unsigned long long c0 = 0, c1 = 0, c2 = 0, w0 = 0, w1 = 0, w2 = 0;
-    for (uint64_t k = k0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < k1;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t v;
-        uint32_t c = dyad_cost(off, adj, __ldg(du + k), __ldg(dp + k), &v);
-        int b = bin_of(c);
-        if (b == 0) { c0++; w0 += c; }
-        else if (b == 1) { c1++; w1 += c; }
-        else { c2 += (c + kBlockSpan - 1) / kBlockSpan; w2 += c; }
-    }
-    for (int o = 16; o; o >>= 1) {
-        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
-        c2 += __shfl_xor_sync(0xffffffffu, c2, o);
-        w0 += __shfl_xor_sync(0xffffffffu, w0, o);
-        w1 += __shfl_xor_sync(0xffffffffu, w1, o);
-        w2 += __shfl_xor_sync(0xffffffffu, w2, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (c0) atomicAdd(&cnt[0], c0);
-        if (c1) atomicAdd(&cnt[1], c1);
-        if (c2) atomicAdd(&cnt[2], c2);
-        if (w0) atomicAdd(&cnt[3], w0);
-        if (w1) atomicAdd(&cnt[4], w1);
-        if (w2) atomicAdd(&cnt[5], w2);
-    }
-}
-
-__global__ void k_plan_fill(const uint32_t *__restrict__ du, const uint32_t *__restrict__ dp,
-                            const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj,
-                            uint64_t k0, uint64_t k1, BinItem2 *tl, BinItem2 *wl, BinItem4 *bl,
-                            unsigned long long *cur) {
-    const uint32_t lane = threadIdx.x & 31, lt = (1u << lane) - 1u;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t base = k0 + ((uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u));
-         base < k1; base += stride) {
-        uint64_t k = base + lane;
-        bool valid = k < k1;
-        uint32_t u = 0, p = 0, v = 0, c = 0;
-        int b = -1;
-        if (valid) {
-            u = __ldg(du + k);
-            p = __ldg(dp + k);
-            c = dyad_cost(off, adj, u, p, &v);
-            b = bin_of(c);
-        }
+// One block per tile of kPlanTile consecutive canonical dyads: a stable
+// tile-local counting sort of the thread-bin dyads by cost c (warp-level
+// __match_any_sync ranking, then a block scan over the 255 cost digits), so
+// the census keeps the tile's row locality and still gives every warp equal
+// trip counts.  Dyads with c > kThreadBinMax become warp items (<= 8160
+// diagonals each) appended through an atomic cursor.
+// stats: [0] warp items, [1] thread-bin work, [2] warp-bin work, [3] big dyads
+__global__ void __launch_bounds__(kPlanThreads)
+k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
+            const uint32_t *__restrict__ dc, uint64_t N, BinItem2 *__restrict__ tl,
+            uint32_t *__restrict__ tile_count, BinItem4 *__restrict__ wl,
+            unsigned long long *__restrict__ stats) {
+    __shared__ uint32_t wc[kPlanWarps][kDigits];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kPlanWarps * kDigits; i += kPlanThreads) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kPlanTile;
+    const uint32_t wbase = warp * 32 * kPlanItems;
+    uint32_t cst[kPlanItems], rank[kPlanItems];
 #pragma unroll
-        for (int q = 0; q < 2; q++) {
-            uint32_t m = __ballot_sync(0xffffffffu, b == q);
-            if (m) {
-                int leader = __ffs(m) - 1;
-                unsigned long long at = 0;
-                if ((int)lane == leader) at = atomicAdd(&cur[q], (unsigned long long)__popc(m));
-                at = __shfl_sync(0xffffffffu, at, leader);
-                if (b == q) {
-                    BinItem2 it{u, p};
-                    (q == 0 ? tl : wl)[at + __popc(m & lt)] = it;
-                }
-            }
+    for (int k = 0; k < kPlanItems; k++) {
+        uint64_t i = tile0 + wbase + k * 32 + lane;
+        bool valid = i < N;
+        cst[k] = valid ? __ldg(dc + i) : 0u;
+        uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t r = 0;
+        if (valid) r = wc[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
+        rank[k] = r;
+    }
+    __syncthreads();
+    {   // thread d owns digit d: tile-local offsets (digit-major, then warp)
+        const int d = threadIdx.x;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kPlanWarps; w++) tot += wc[w][d];
+        if (d == 255) tot = 0;      // big dyads are not in the thread list
+        uint32_t all;
+        uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
+        if (d == 0) tile_count[blockIdx.x] = all;
+#pragma unroll
+        for (int w = 0; w < kPlanWarps; w++) {
+            uint32_t c = wc[w][d];
+            wc[w][d] = run;
+            run += c;
         }
-        if (b == 2) {
-            uint32_t nch = (c + kBlockSpan - 1) / kBlockSpan;
-            unsigned long long at = atomicAdd(&cur[2], (unsigned long long)nch);
+    }
+    __syncthreads();
+    BinItem2 *out = tl + tile0;
+    unsigned long long wt = 0, ww = 0, nbig = 0;
+#pragma unroll
+    for (int k = 0; k < kPlanItems; k++) {
+        uint64_t i = tile0 + wbase + k * 32 + lane;
+        if (i >= N) continue;
+        uint32_t c = cst[k], d = digit_of(c);
+        uint32_t u = __ldg(du + i), e = __ldg(de + i);
+        if (d < 255u) {
+            out[wc[warp][d] + rank[k]] = BinItem2{u, e};
+            wt += c;
+        } else {
+            uint32_t nch = (c + kWarpChunk - 1) / kWarpChunk;
+            unsigned long long at = atomicAdd(&stats[0], (unsigned long long)nch);
             for (uint32_t q = 0; q < nch; q++) {
-                uint32_t d0 = q * kBlockSpan, d1 = min(c, d0 + kBlockSpan);
-                bl[at + q] = BinItem4{u, p, d0, d1};
+                uint32_t d0 = q * kWarpChunk;
+                wl[at + q] = BinItem4{u, e, d0, min(c, d0 + kWarpChunk)};
             }
+            ww += c;
+            nbig++;
         }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        wt += __shfl_xor_sync(0xffffffffu, wt, o);
+        ww += __shfl_xor_sync(0xffffffffu, ww, o);
+        nbig += __shfl_xor_sync(0xffffffffu, nbig, o);
+    }
+    if (lane == 0) {
+        if (wt) atomicAdd(&stats[1], wt);
+        if (ww) atomicAdd(&stats[2], ww);
+        if (nbig) atomicAdd(&stats[3], nbig);
     }
 }
 
 struct CostIn {
-    const uint32_t *du, *dp, *off, *adj;
+    const uint32_t *dc;
     uint64_t kappa;
     __device__ __forceinline__ uint64_t operator()(size_t k) const {
-        uint32_t v;
-        return (uint64_t)dyad_cost(off, adj, __ldg(du + k), __ldg(dp + k), &v) + kappa;
+        return (uint64_t)__ldg(dc + k) + kappa;
     }
 };
 
@@ -127,13 +138,6 @@ __global__ void k_lower_bounds(const uint64_t *__restrict__ excl, uint64_t D,
     out[r] = lo;
 }
 
-inline unsigned grid_for(uint64_t work, int threads, unsigned cap = 148 * 16) {
-    uint64_t b = (work + threads - 1) / threads;
-    if (b < 1) b = 1;
-    if (b > cap) b = cap;
-    return (unsigned)b;
-}
-
 }  // namespace
 
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
@@ -141,52 +145,71 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     const uint64_t D = g->st.dyads;
     if (k1 > D) k1 = D;
     if (k0 >= k1) return TC_OK;
+    const uint64_t N = k1 - k0;
+    if (N >= (1ull << 32)) {
+        set_error("dyad range too large");
+        return TC_E_INVALID;
+    }
     Mem mem = g->mem;
     mem.stream = s;
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     if (prof) {
-        TC_CUDA(cudaEventCreate(&e0));
-        TC_CUDA(cudaEventCreate(&e1));
-        TC_CUDA(cudaEventRecord(e0, s));
+        for (int i = 0; i < 4; i++) TC_CUDA(cudaEventCreate(&ev[i]));
+        TC_CUDA(cudaEventRecord(ev[0], s));
     }
     tc_status st;
-    DevBuf<unsigned long long> cnt;
-    if ((st = cnt.allocate(mem, 12)) != TC_OK) return st;
-    TC_CUDA(cudaMemsetAsync(cnt.p, 0, 12 * sizeof(unsigned long long), s));
-    k_plan_count<<<grid_for(k1 - k0, 256), 256, 0, s>>>(g->dyad_u, g->dyad_p, g->off, g->adj, k0,
-                                                        k1, cnt.p);
+    const uint64_t ntiles = (N + kPlanTile - 1) / kPlanTile;
+    // upper bound on warp items: sum over big dyads of ceil(c / chunk)
+    const uint64_t nbig_max = g->st.sum_deg_sq / (kThreadBinMax + 1) + 1;
+    const uint64_t wcap = (nbig_max < N ? nbig_max : N) + g->st.sum_deg_sq / kWarpChunk + 2;
+    DevBuf<uint32_t> tcount;
+    DevBuf<BinItem2> tl;
+    DevBuf<BinItem4> wl;
+    DevBuf<unsigned long long> stats;
+    if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
+    if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
+    if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
+    if ((st = stats.allocate(mem, 4)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(stats.p, 0, 4 * sizeof(unsigned long long), s));
+    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(g->dyad_u + k0, g->dyad_e + k0,
+                                                          g->dyad_c + k0, N, tl.p, tcount.p,
+                                                          wl.p, stats.p);
     TC_CUDA(cudaGetLastError());
-    unsigned long long h[6];
-    TC_CUDA(cudaMemcpyAsync(h, cnt.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    DevBuf<BinItem2> tl, wl;
-    DevBuf<BinItem4> bl;
-    if ((st = tl.allocate(mem, h[0])) != TC_OK) return st;
-    if ((st = wl.allocate(mem, h[1])) != TC_OK) return st;
-    if ((st = bl.allocate(mem, h[2])) != TC_OK) return st;
-    k_plan_fill<<<grid_for(k1 - k0, 256), 256, 0, s>>>(g->dyad_u, g->dyad_p, g->off, g->adj, k0,
-                                                       k1, tl.p, wl.p, bl.p, cnt.p + 6);
-    TC_CUDA(cudaGetLastError());
-    *launches += 2;
-    if (prof) {
-        TC_CUDA(cudaEventRecord(e1, s));
-        TC_CUDA(cudaEventSynchronize(e1));
-        float t;
-        TC_CUDA(cudaEventElapsedTime(&t, e0, e1));
-        prof->plan_ms = t;
-        for (int i = 0; i < 3; i++) {
-            prof->bin_items[i] = h[i];
-            prof->bin_work[i] = h[3 + i];
-        }
-        cudaEventDestroy(e0);
-        cudaEventDestroy(e1);
-    }
+    *launches += 1;
     BinLists lists;
     lists.t = tl.p;
+    lists.t_count = tcount.p;
+    lists.ntiles = ntiles;
     lists.w = wl.p;
-    lists.b = bl.p;
-    for (int i = 0; i < 3; i++) lists.count[i] = h[i];
-    return launch_bins(g, lists, s, d_counts, prof, launches);
+    lists.w_count = stats.p;
+    st = launch_bins(g, lists, s, d_counts, prof ? ev + 1 : nullptr, launches);
+    if (st != TC_OK) return st;
+    if (prof) {
+        TC_CUDA(cudaEventRecord(ev[3], s));
+        unsigned long long hs[4];
+        TC_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        const uint64_t nt = N - hs[3];
+        float t;
+        TC_CUDA(cudaEventElapsedTime(&t, ev[0], ev[1]));
+        prof->plan_ms = t;
+        TC_CUDA(cudaEventElapsedTime(&t, ev[1], ev[2]));
+        prof->kernel_ms[0] = t;
+        TC_CUDA(cudaEventElapsedTime(&t, ev[2], ev[3]));
+        prof->kernel_ms[1] = t;
+        prof->kernel_ms[2] = prof->kernel_ms[3] = 0;
+        TC_CUDA(cudaEventElapsedTime(&t, ev[1], ev[3]));
+        prof->census_ms = t;
+        prof->bin_items[0] = nt;
+        prof->bin_items[1] = hs[0];
+        prof->bin_items[2] = hs[3];   // dyads in the warp bin
+        prof->bin_items[3] = 0;
+        prof->bin_work[0] = hs[1];
+        prof->bin_work[1] = hs[2];
+        prof->bin_work[2] = prof->bin_work[3] = 0;
+        for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
+    }
+    return TC_OK;
 }
 
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
@@ -195,23 +218,23 @@ tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint
     bounds[0] = 0;
     bounds[world] = D;
     if (world == 1) return TC_OK;
+    if (world > 1024) {
+        set_error("world %d > 1024", world);
+        return TC_E_INVALID;
+    }
     Mem mem = g->mem;
     mem.stream = s;
     tc_status st;
     DevBuf<uint64_t> excl, tot, tg, out;
     if ((st = excl.allocate(mem, D)) != TC_OK) return st;
     if ((st = tot.allocate(mem, 1)) != TC_OK) return st;
-    st = scan_exclusive<uint64_t>(mem, D, CostIn{g->dyad_u, g->dyad_p, g->off, g->adj, kappa},
-                                  ArrayOutExcl<uint64_t>{excl.p}, tot.p, s, nullptr);
+    st = scan_exclusive<uint64_t>(mem, D, CostIn{g->dyad_c, kappa}, ArrayOutExcl<uint64_t>{excl.p},
+                                  tot.p, s, nullptr);
     if (st != TC_OK) return st;
     uint64_t T = 0;
     TC_CUDA(cudaMemcpyAsync(&T, tot.p, sizeof(T), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     uint64_t targets[1024];
-    if (world > 1024) {
-        set_error("world %d > 1024", world);
-        return TC_E_INVALID;
-    }
     for (int r = 1; r < world; r++)
         targets[r - 1] = (uint64_t)(((unsigned __int128)T * (unsigned)r) / (unsigned)world);
     if ((st = tg.allocate(mem, world)) != TC_OK) return st;

@@ -4,9 +4,11 @@
 //   off[n+1]   uint32 row offsets of the symmetric neighbour CSR
 //   adj[2D]    uint32 entries (w << 2) | tag, each row sorted by w;
 //              tag bit0 = u->w, bit1 = w->u (the 2-bit direction code)
-//   dyad_u[D], dyad_p[D]   canonical dyads (u < v) in canonical order
-//              (u ascending, v ascending): row u and the CSR
-//              position p of v in row u (so v = adj[p] >> 2, pre = adj[p] & 3)
+//   dyad_u[D], dyad_e[D], dyad_c[D]   canonical dyads (u < v) in canonical
+//              order (u ascending, v ascending): row u, the entry
+//              of v in row u, e = (v << 2) | pre with pre = IsEdge(u,v) +
+//              2 IsEdge(v,u) (v0.4), and the uniform cost
+//              c = |N(u)| + |N(v)|
 #pragma once
 
 #include <cuda_runtime.h>
@@ -68,20 +70,19 @@ struct DevBuf {
 // ---------------------------------------------------------------------------
 // bin thresholds of the degree-binned scheduler (a2).  Cost c = |N(u)|+|N(v)|.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kThreadBinMax = 96;     // c <= 96: one thread per dyad
-constexpr uint32_t kWarpBinMax = 4096;     // c <= 4096: one warp per dyad
-constexpr uint32_t kBlockThreads = 256;    // block bin: 256 threads per chunk
-constexpr uint32_t kBlockSpan = 8192;      // diagonals per block-bin chunk
-constexpr int kNumBins = 3;
+constexpr uint32_t kThreadBinMax = 254;    // c <= 254: one thread per dyad, sorted by c
+constexpr uint32_t kLaneSpan = 255;        // max diagonals per lane (8-bit packed counters)
+constexpr uint32_t kWarpChunk = 32 * kLaneSpan;   // c > 254: warp items of <= 8160 diagonals
+constexpr int kNumBins = 2;
 // per-dyad overhead of the shard cost model, in list-entry equivalents
 // (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
 constexpr uint64_t kShardKappa = 8;
 
-struct BinItem2 {   // thread / warp bins
-    uint32_t u, p;
+struct BinItem2 {   // thread bin: dyad (u, e)
+    uint32_t u, e;
 };
-struct BinItem4 {   // block bin: dyad (u, p) and merge diagonals [d0, d1)
-    uint32_t u, p, d0, d1;
+struct BinItem4 {   // warp bin: dyad (u, e) and its merge diagonals [d0, d1)
+    uint32_t u, e, d0, d1;
 };
 
 }  // namespace tc
@@ -95,7 +96,8 @@ struct tc_graph {
     uint32_t *off = nullptr;   size_t off_n = 0;
     uint32_t *adj = nullptr;   size_t adj_n = 0;
     uint32_t *dyad_u = nullptr; size_t dyad_n = 0;
-    uint32_t *dyad_p = nullptr;
+    uint32_t *dyad_e = nullptr;
+    uint32_t *dyad_c = nullptr;
     int profile = 0;
     tc_profile prof{};
     uint64_t launches = 0;
