@@ -197,3 +197,15 @@ def test_errors(tcb):
         tcb.tc_graph_create(5, np.array([0, 7, 1], np.uint32), np.array([1, 0, 2], np.uint32))
     with pytest.raises(tcb.TCError, match="TC_E_INVALID"):
         tcb.tc_graph_create(2**30, np.zeros(0, np.uint32), np.zeros(0, np.uint32))
+
+
+def test_census_multi_world1_nccl(tcb):
+    # tc_census_multi through a 1-rank NCCL communicator equals tc_census
+    a = synth.make_config("C2")
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    comm = tcb.tc_comm_create(tcb.tc_comm_unique_id(), 1, 0, 0)
+    try:
+        assert tcb.tc_census_multi(g, comm) == g.census()
+    finally:
+        comm.close()
+        g.close()
