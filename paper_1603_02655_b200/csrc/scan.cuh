@@ -25,9 +25,9 @@ __device__ __forceinline__ T warp_inclusive_sum(T x) {
 
 // Exclusive scan of one value per thread across the block (blockDim.x ==
 // kScanThreads).  Returns the thread's exclusive prefix; *total = block sum.
-template <typename T>
+template <typename T, int NT = kScanThreads>
 __device__ __forceinline__ T block_exclusive_sum(T x, T *total) {
-    constexpr int NW = kScanThreads / 32;
+    constexpr int NW = NT / 32;
     __shared__ T warp_sums[NW];
     __shared__ T block_total;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

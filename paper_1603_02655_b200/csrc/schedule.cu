@@ -32,7 +32,7 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t c) {
 
 // One block per tile of kPlanTile consecutive canonical dyads: a stable
 // tile-local counting sort of the thread-bin dyads by cost c (warp-level
-// __match_any_sync ranking, then a block scan over the 255 cost digits), so
+// ballot ranking, then a block scan over the 255 cost digits), so
 // the census keeps the tile's row locality and still gives every warp equal
 // trip counts.  Dyads with c > kThreadBinMax become warp items (<= 8160
 // diagonals each) appended through an atomic cursor.
@@ -56,7 +56,13 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
         bool valid = i < N;
         cst[k] = valid ? __ldg(dc + i) : 0u;
         uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        // lanes holding the same digit: one ballot per digit bit
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bit = 0; bit < 8; bit++) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+            peers &= ((d >> bit) & 1u) ? b : ~b;
+        }
         uint32_t r = 0;
         if (valid) r = wc[warp][d] + __popc(peers & lt);
         __syncwarp();
@@ -73,7 +79,10 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
         if (d == 255) tot = 0;      // big dyads are not in the thread list
         uint32_t all;
         uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
-        if (d == 0) tile_count[blockIdx.x] = all;
+        // tile meta: [0] thread-bin items, [1] items with c <= 64, [2] c <= 128
+        if (d == 0) tile_count[4 * blockIdx.x] = all;
+        if (d == kSeg1Max + 1) tile_count[4 * blockIdx.x + 1] = run;
+        if (d == kSeg2Max + 1) tile_count[4 * blockIdx.x + 2] = run;
 #pragma unroll
         for (int w = 0; w < kPlanWarps; w++) {
             uint32_t c = wc[w][d];
@@ -166,7 +175,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     DevBuf<BinItem2> tl;
     DevBuf<BinItem4> wl;
     DevBuf<unsigned long long> stats;
-    if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
+    if ((st = tcount.allocate(mem, 4 * ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
     if ((st = stats.allocate(mem, 4)) != TC_OK) return st;
