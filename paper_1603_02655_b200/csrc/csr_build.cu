@@ -74,10 +74,9 @@ __device__ __forceinline__ void head_flags(const uint64_t *__restrict__ key, siz
     canon = head && key_row(k) < key_col(k);
 }
 
-// pass 1: per tile, number of heads | canonical heads << 32
+// pass 1: per warp (512 keys), number of heads | canonical heads << 32
 __global__ void __launch_bounds__(kHcThreads)
-k_head_count(const uint64_t *__restrict__ key, size_t L, uint64_t *__restrict__ tile_tot) {
-    __shared__ uint64_t wsum[kHcWarps];
+k_head_count(const uint64_t *__restrict__ key, size_t L, uint64_t *__restrict__ warp_tot) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
     uint32_t nh = 0, nc = 0;
@@ -89,38 +88,19 @@ k_head_count(const uint64_t *__restrict__ key, size_t L, uint64_t *__restrict__ 
         nh += __popc(__ballot_sync(0xffffffffu, head));
         nc += __popc(__ballot_sync(0xffffffffu, canon));
     }
-    if (lane == 0) wsum[warp] = (uint64_t)nh | ((uint64_t)nc << 32);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        uint64_t t = 0;
-        for (int w = 0; w < kHcWarps; w++) t += wsum[w];
-        tile_tot[blockIdx.x] = t;
-    }
+    if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = (uint64_t)nh | ((uint64_t)nc << 32);
 }
 
 // pass 2: write adj / dyad lists / row offsets at the compacted positions
+// (warp_off = exclusive scan of pass 1's per-warp totals)
 __global__ void __launch_bounds__(kHcThreads)
-k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restrict__ tile_off,
+k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restrict__ warp_off,
              uint32_t *__restrict__ adj, uint32_t *__restrict__ du, uint32_t *__restrict__ de,
              uint32_t *__restrict__ off) {
-    __shared__ uint64_t wsum[kHcWarps];
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
-    // warp totals (L1-hot re-read of the warp's 512 keys) -> warp offsets
-    uint32_t nh = 0, nc = 0;
-#pragma unroll 4
-    for (int r = 0; r < kHcItems; r++) {
-        uint64_t k, prev;
-        bool head, canon;
-        head_flags(key, L, base + (size_t)r * 32 + lane, k, prev, head, canon);
-        nh += __popc(__ballot_sync(0xffffffffu, head));
-        nc += __popc(__ballot_sync(0xffffffffu, canon));
-    }
-    if (lane == 0) wsum[warp] = (uint64_t)nh | ((uint64_t)nc << 32);
-    __syncthreads();
-    uint64_t woff = tile_off[blockIdx.x];
-    for (uint32_t w = 0; w < warp; w++) woff += wsum[w];
+    const uint64_t woff = warp_off[(size_t)blockIdx.x * kHcWarps + warp];
     uint32_t r0 = (uint32_t)woff, k0 = (uint32_t)(woff >> 32);
     for (int r = 0; r < kHcItems; r++) {
         const size_t i = base + (size_t)r * 32 + lane;
@@ -129,14 +109,21 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restr
         head_flags(key, L, i, k, prev, head, canon);
         const uint32_t bh = __ballot_sync(0xffffffffu, head);
         const uint32_t bc = __ballot_sync(0xffffffffu, canon);
+        // next key (lane + 1, or a load for lane 31) for the run's tag OR
+        uint64_t nxt = __shfl_down_sync(0xffffffffu, k, 1);
+        if (lane == 31) nxt = i + 1 < L ? __ldg(key + i + 1) : kSentinel;
         if (head) {
             const uint32_t rr = r0 + __popc(bh & lt);
             const uint32_t row = key_row(k), col = key_col(k);
             uint32_t tag = (uint32_t)(k & 3u);
-            for (size_t j = i + 1; j < L; j++) {       // OR the run's tags
-                uint64_t kj = __ldg(key + j);
-                if ((kj >> 2) != (k >> 2)) break;
-                tag |= (uint32_t)(kj & 3u);
+            if ((nxt >> 2) == (k >> 2)) {            // mutual pair and/or duplicates
+                tag |= (uint32_t)(nxt & 3u);
+#pragma unroll 1
+                for (size_t j = i + 2; j < L && tag != 3u; j++) {   // longer runs: duplicates
+                    const uint64_t kj = __ldg(key + j);
+                    if ((kj >> 2) != (k >> 2)) break;
+                    tag |= (uint32_t)(kj & 3u);
+                }
             }
             const uint32_t e = (col << 2) | tag;
             adj[rr + row] = e;
@@ -146,14 +133,12 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restr
                 de[kk] = e;
             }
             // first entry of row `row`: rows (prev_row, row] start here
-            uint32_t first = 0;
-            bool boundary = (i == 0);
-            if (!boundary && key_row(prev) != row) {
-                boundary = true;
-                first = key_row(prev) + 1;
+            if (i == 0 || key_row(prev) != row) {
+                off[row] = rr + row;
+                const uint32_t first = i == 0 ? 0u : key_row(prev) + 1;
+#pragma unroll 1
+                for (uint32_t x = first; x < row; x++) off[x] = rr + x;   // empty rows
             }
-            if (boundary)
-                for (uint32_t x = first; x <= row; x++) off[x] = rr + x;
         }
         r0 += __popc(bh);
         k0 += __popc(bc);
@@ -237,8 +222,8 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     Mem &mem = g->mem;
 
     DevBuf<unsigned long long> scratch;
-    if ((st = scratch.allocate(mem, 8)) != TC_OK) return st;
-    unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+    if ((st = scratch.allocate(mem, 16)) != TC_OK) return st;
+    unsigned long long init[16] = {~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     TC_CUDA(cudaMemcpyAsync(scratch.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
 
     size_t L0 = 2 * (size_t)m;
@@ -297,11 +282,11 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     if (L) {
         const size_t ntiles = (L + kHcTile - 1) / kHcTile;
         DevBuf<uint64_t> tt, total;
-        if ((st = tt.allocate(mem, ntiles)) != TC_OK) return st;
+        if ((st = tt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
         if ((st = total.allocate(mem, 1)) != TC_OK) return st;
         k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p);
         TC_CUDA(cudaGetLastError());
-        st = scan_exclusive<uint64_t>(mem, ntiles, ArrayIn<uint64_t>{tt.p},
+        st = scan_exclusive<uint64_t>(mem, ntiles * kHcWarps, ArrayIn<uint64_t>{tt.p},
                                       ArrayOutExcl<uint64_t>{tt.p}, total.p, s, &g->launches);
         if (st != TC_OK) return st;
         k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p, adj, du, de, off);
