@@ -34,9 +34,6 @@
 // classes), which a warp flushes (REDUX sum per class) into per-warp shared
 // totals before they can overflow; blocks end with one global atomicAdd per
 // class.
-#include <stdlib.h>
-#include <string.h>
-
 #include "census.cuh"
 
 namespace tc {
@@ -227,7 +224,7 @@ k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t cnt = __ldg(tile_count + 4 * tile);
+        const uint32_t cnt = __ldg(tile_count + tile);
         const BinItem2 *it = items + tile * kPlanTile;
         for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
@@ -249,188 +246,6 @@ k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__
         }
     }
     block_finish(c, wsh, d_counts);
-}
-
-// ---------------------------------------------------------------------------
-// Thread bin, TMA-staged (default): each warp takes batches of dyads of its
-// block's tile (cost-sorted segments c <= 64 / <= 128 / <= 254 with G = 1 / 2
-// / 4 lanes per dyad, so every lane merges <= 64 diagonals).  The group
-// leader lane issues two bulk copies (cp.async.bulk, the TMA engine) of the
-// 16-byte-aligned supersets of N(u) and N(v) (sentinels included) into the
-// warp's shared buffer; completion is tracked by a per-warp mbarrier
-// (expect_tx).  The merge then reads only shared memory: no lane waits on a
-// global load inside the loop, so one slow row no longer stalls a warp trip.
-// ---------------------------------------------------------------------------
-constexpr uint32_t kStageEntries = 2560;          // u32 per warp buffer (10 KB)
-constexpr int kTmaThreads = 256;
-constexpr int kTmaWarps = kTmaThreads / 32;
-
-struct TmaSmem {
-    uint32_t buf[kTmaWarps][kStageEntries];
-    unsigned long long wsh[kTmaWarps][16];
-    unsigned long long mbar[kTmaWarps];
-    uint32_t next[3];                             // per-segment batch cursors
-    uint8_t tab[64];
-};
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t phase) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "W%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra W%=;\n}" ::"r"(bar), "r"(phase) : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(uint32_t dst, const void *src, uint32_t bytes,
-                                            uint32_t bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
-}
-__device__ __forceinline__ uint32_t lds_at(uint32_t base, uint32_t idx) {
-    uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 4u * idx) : "memory");
-    return v;
-}
-
-// merge-path split over shared rows A (a entries) and B (b entries)
-__device__ __forceinline__ uint32_t merge_path_s(uint32_t A, uint32_t a, uint32_t B, uint32_t b,
-                                                 uint32_t d) {
-    uint32_t lo = d > b ? d - b : 0u, hi = d < a ? d : a;
-    while (lo < hi) {
-        uint32_t mid = (lo + hi) >> 1;
-        if ((lds_at(A, mid) | 3u) <= (lds_at(B, d - mid - 1) | 3u)) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
-// merge_diag over rows staged in shared memory (sentinel after each row)
-__device__ __forceinline__ void merge_diag_s(uint32_t A, uint32_t a, uint32_t B, uint32_t b,
-                                             uint32_t ku, uint32_t kv, uint32_t pre, uint32_t d0,
-                                             uint32_t d1, uint32_t tab, Acc &c) {
-    uint32_t i = 0;
-    if (d0 > 0) i = merge_path_s(A, a, B, b, d0);
-    uint32_t j = d0 - i;
-    uint32_t lastA = i > 0 ? (lds_at(A, i - 1) | 3u) : 0u;
-    uint32_t x = lds_at(A, i), y = lds_at(B, j);
-    uint32_t I = 0;
-    const uint32_t tabp = tab + pre;
-    uint32_t t = d0;
-    while (t < d1) {
-        const uint32_t lim = min(d1, t + 15u);   // nibble counters hold 15
-        for (; t < lim; t++) {
-            const uint32_t kx = x | 3u, ky = y | 3u;
-            const bool ta = kx <= ky;
-            const bool tb = ky <= kx;
-            const uint32_t ca = ta ? ((x << 2) & 12u) : 0u;
-            const uint32_t cb = tb ? ((y << 4) & 48u) : 0u;
-            const bool canon = ta ? (kx > kv) : ((ky != lastA) & (ky > ku));
-            I += (uint32_t)(ta & tb);
-            const uint32_t sh = canon ? lds_u8(tabp + (ca | cb)) : 0u;
-            c.n4 += 1ull << sh;
-            lastA = ta ? kx : lastA;
-            i += ta;
-            j += !ta;
-            const uint32_t nv = ta ? lds_at(A, i) : lds_at(B, j);
-            x = ta ? nv : x;
-            y = ta ? y : nv;
-        }
-        spill(c);
-    }
-    add_dyadic(c, pre, I);
-}
-
-__global__ void __launch_bounds__(kTmaThreads)
-k_census_tma(const BinItem2 *__restrict__ items, const uint32_t *__restrict__ tile_meta,
-             uint64_t ntiles, const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj,
-             uint64_t n, unsigned long long *d_counts) {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    TmaSmem &S = *reinterpret_cast<TmaSmem *>(smem_raw);
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (threadIdx.x < 64) S.tab[threadIdx.x] = (uint8_t)(4u * c_triad_table[threadIdx.x]);
-    for (int i = threadIdx.x; i < kTmaWarps * 16; i += blockDim.x) (&S.wsh[0][0])[i] = 0;
-    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&S.mbar[warp]);
-    if (lane == 0) mbar_init(bar, 32);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    __syncthreads();
-    const uint32_t tab = (uint32_t)__cvta_generic_to_shared(S.tab);
-    const uint32_t wbuf = (uint32_t)__cvta_generic_to_shared(&S.buf[warp][0]);
-    uint32_t phase = 0;
-    Acc c;
-    acc_init(c);
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t cnt = __ldg(tile_meta + 4 * tile);
-        const uint32_t s1 = __ldg(tile_meta + 4 * tile + 1), s2 = __ldg(tile_meta + 4 * tile + 2);
-        if (threadIdx.x < 3) S.next[threadIdx.x] = 0;
-        __syncthreads();
-        const BinItem2 *it = items + tile * kPlanTile;
-        const uint32_t seg_lo[3] = {0u, s1, s2}, seg_hi[3] = {s1, s2, cnt};
-#pragma unroll 1
-        for (int sg = 0; sg < 3; sg++) {
-            const uint32_t lg = sg;                 // log2(G)
-            const uint32_t G = 1u << lg, k = 32u >> lg;
-            const uint32_t lo = seg_lo[sg], hi = seg_hi[sg];
-            for (;;) {
-                uint32_t b0 = 0;
-                if (lane == 0) b0 = atomicAdd(&S.next[sg], k);
-                b0 = __shfl_sync(0xffffffffu, b0, 0) + lo;
-                if (b0 >= hi) break;
-                const uint32_t slot = lane >> lg, g = lane & (G - 1u);
-                const bool valid = b0 + slot < hi;
-                BinItem2 e{0, 0};
-                uint32_t ou = 0, a = 0, ov = 0, b = 0;
-                if (valid) {
-                    e = it[b0 + slot];
-                    row_of(off, e.u, ou, a);
-                    row_of(off, e.e >> 2, ov, b);
-                }
-                // 16-byte aligned supersets [floor4(o), ceil4(o + len + 1)) of both rows
-                const uint32_t fa = ou & ~3u, fb = ov & ~3u;
-                const uint32_t na = valid ? ((ou + a + 4u) & ~3u) - fa : 0u;
-                const uint32_t nb = valid ? ((ov + b + 4u) & ~3u) - fb : 0u;
-                const bool leader = valid && g == 0;
-                uint32_t need = leader ? na + nb : 0u, incl = need;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if ((int)lane >= o) incl += y;
-                }
-                uint32_t sdst = incl - need;        // leader's offset in the warp buffer
-                sdst = __shfl_sync(0xffffffffu, sdst, lane & ~(G - 1u));
-                // the buffer was last read through the generic proxy; order
-                // those reads before the async-proxy (TMA) writes
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive_tx(bar, need * 4u);
-                if (leader) {
-                    tma_load_1d(wbuf + 4u * sdst, adj + fa, na * 4u, bar);
-                    tma_load_1d(wbuf + 4u * (sdst + na), adj + fb, nb * 4u, bar);
-                }
-                mbar_wait(bar, phase);
-                phase ^= 1u;
-                const uint32_t cst = a + b, per = (cst + G - 1u) >> lg;
-                const uint32_t d0 = min(cst, g * per), d1 = min(cst, d0 + per);
-                warp_reserve(c, S.wsh[warp], d1 - d0);
-                if (valid) {
-                    const uint32_t pre = e.e & 3u;
-                    if (g == 0) add_dyadic(c, pre, n - a - b);
-                    if (d0 < d1)
-                        merge_diag_s(wbuf + 4u * (sdst + (ou & 3u)), a,
-                                     wbuf + 4u * (sdst + na + (ov & 3u)), b, (e.u << 2) | 3u,
-                                     e.e | 3u, pre, d0, d1, tab, c);
-                }
-                __syncwarp();
-            }
-        }
-        __syncthreads();
-    }
-    block_finish(c, S.wsh, d_counts);
 }
 
 // warp bin: one warp per item = one dyad's diagonals [d0, d1), 32 lane
@@ -476,16 +291,8 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     const unsigned grid = (unsigned)sms * kCensusBlocksPerSM;
     const size_t dyn = 0;
     if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
-    static const bool legacy = !(getenv("TC_THREAD_KERNEL") && !strcmp(getenv("TC_THREAD_KERNEL"), "tma"));
-    if (legacy) {
-        k_census_thread<<<grid, kCensusThreads, dyn, s>>>(bl.t, bl.t_count, bl.ntiles, g->off,
-                                                         g->adj, n, out);
-    } else {
-        TC_CUDA(cudaFuncSetAttribute(k_census_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(TmaSmem)));
-        k_census_tma<<<(unsigned)sms * 2, kTmaThreads, sizeof(TmaSmem), s>>>(
-            bl.t, bl.t_count, bl.ntiles, g->off, g->adj, n, out);
-    }
+    k_census_thread<<<grid, kCensusThreads, dyn, s>>>(bl.t, bl.t_count, bl.ntiles, g->off, g->adj,
+                                                     n, out);
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
     k_census_warp<<<grid, kCensusThreads, 0, s>>>(bl.w, bl.w_count, g->off, g->adj, n, out);

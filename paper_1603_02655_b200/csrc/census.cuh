@@ -8,7 +8,7 @@ namespace tc {
 // the census need no host round trip.
 struct BinLists {
     const BinItem2 *t = nullptr;            // thread bin: tile-local lists sorted by cost
-    const uint32_t *t_count = nullptr;      // device: per tile {items, #c<=64, #c<=128, -}
+    const uint32_t *t_count = nullptr;      // device: thread-bin items per tile
     uint64_t ntiles = 0;                    // tiles of kPlanTile canonical dyads
     const BinItem4 *w = nullptr;            // warp bin: <= kWarpChunk diagonals per item
     const unsigned long long *w_count = nullptr;   // device: number of warp-bin items
@@ -19,9 +19,7 @@ constexpr int kPlanThreads = 256;
 constexpr int kPlanItems = 16;
 constexpr int kPlanTile = kPlanThreads * kPlanItems;   // canonical dyads per plan tile
 constexpr unsigned kCensusBlocksPerSM = 8;
-// thread-bin cost segments: lanes per dyad G = 1 (c <= 64), 2 (c <= 128), 4
-constexpr uint32_t kSeg1Max = 64;
-constexpr uint32_t kSeg2Max = 128;
+
 
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,

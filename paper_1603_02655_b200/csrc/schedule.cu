@@ -79,10 +79,7 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
         if (d == 255) tot = 0;      // big dyads are not in the thread list
         uint32_t all;
         uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
-        // tile meta: [0] thread-bin items, [1] items with c <= 64, [2] c <= 128
-        if (d == 0) tile_count[4 * blockIdx.x] = all;
-        if (d == kSeg1Max + 1) tile_count[4 * blockIdx.x + 1] = run;
-        if (d == kSeg2Max + 1) tile_count[4 * blockIdx.x + 2] = run;
+        if (d == 0) tile_count[blockIdx.x] = all;
 #pragma unroll
         for (int w = 0; w < kPlanWarps; w++) {
             uint32_t c = wc[w][d];
@@ -175,7 +172,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     DevBuf<BinItem2> tl;
     DevBuf<BinItem4> wl;
     DevBuf<unsigned long long> stats;
-    if ((st = tcount.allocate(mem, 4 * ntiles)) != TC_OK) return st;
+    if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
     if ((st = stats.allocate(mem, 4)) != TC_OK) return st;
