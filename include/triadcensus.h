@@ -189,6 +189,21 @@ tc_status tc_profile_get(const tc_graph *g, tc_profile *out);
  * bench's gpu_launches claim). */
 uint64_t tc_launch_count(const tc_graph *g);
 
+/* Graph file reader (host, the step before the
+ * path).  format: 0 auto (Pajek if the first non-comment line starts with
+ * '*'), 1 Pajek (`*Vertices N` 1-based, `*Arcs` directed, `*Edges` -> two
+ * arcs, `%` comments, trailing label/weight tokens ignored),
+ * 2 edge list ("u v" per line, `#` comments, exactly two integer tokens;
+ * S:152).  index_base: -1 auto (edge lists: 0 if any id is 0, else 1),
+ * 0 or 1 forced (edge lists only).  On success *n, *m and two malloc'ed
+ * 0-based arrays *src, *dst (release with tc_free_arcs).  Errors:
+ * TC_E_INVALID (unreadable file, malformed record -- the message names the
+ * line), TC_E_RANGE (id outside [1, N] in Pajek, 0 in a one-based list),
+ * TC_E_OOM. */
+tc_status tc_read_arcs(const char *path, int format, int index_base, uint64_t *n, uint32_t **src,
+                       uint32_t **dst, uint64_t *m);
+void tc_free_arcs(uint32_t *p);
+
 const char *tc_last_error(void);
 int tc_abi_version(void);
 

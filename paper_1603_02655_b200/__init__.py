@@ -23,7 +23,7 @@ from ._lib import TCError, check, lib
 CLASS_NAMES = ("003", "012", "102", "021D", "021U", "021C", "111D", "111U",
                "030T", "030C", "201", "120D", "120U", "120C", "210", "300")
 
-__all__ = ["CLASS_NAMES", "Graph", "TCError", "tc_graph_create", "tc_census", "tc_census_range",
+__all__ = ["tc_read_arcs", "census_file", "CLASS_NAMES", "Graph", "TCError", "tc_graph_create", "tc_census", "tc_census_range",
            "tc_census_enqueue", "tc_census_multi", "tc_close_census", "tc_shard_bounds",
            "tc_shard_bounds_host", "tc_comm_create", "tc_comm_unique_id", "Comm",
            "census", "lib"]
@@ -253,3 +253,46 @@ def census(n: int, src, dst, device: int = 0) -> list[int]:
         return tc_census(g)
     finally:
         g.close()
+
+
+def tc_read_arcs(path: str, fmt: str = "auto", index_base=None):
+    """Read a Pajek (.net) or SNAP edge-list file with the library's native
+    reader.  Returns (n, src, dst) with 0-based uint32 numpy arrays."""
+    f = {"auto": 0, "pajek": 1, "edgelist": 2}[fmt]
+    b = -1 if index_base is None else int(index_base)
+    n = ctypes.c_uint64(0)
+    m = ctypes.c_uint64(0)
+    ps, pd = _lib.u32p(), _lib.u32p()
+    check(lib.tc_read_arcs(str(path).encode(), f, b, ctypes.byref(n), ctypes.byref(ps),
+                           ctypes.byref(pd), ctypes.byref(m)), "tc_read_arcs")
+    try:
+        k = int(m.value)
+        src = np.ctypeslib.as_array(ps, shape=(k,)).copy() if k else np.zeros(0, np.uint32)
+        dst = np.ctypeslib.as_array(pd, shape=(k,)).copy() if k else np.zeros(0, np.uint32)
+    finally:
+        lib.tc_free_arcs(ps)
+        lib.tc_free_arcs(pd)
+    return int(n.value), src, dst
+
+
+def census_file(path: str, fmt: str = "auto", index_base=None, device: int = 0):
+    """Read a graph file, build, census; returns (counts, timing breakdown in
+    seconds) with the phases of the paper's tables:
+    read graph, CSR build (neighbour sets), plan (task queues), census."""
+    import time
+    torch = _torch()
+    t0 = time.perf_counter()
+    n, src, dst = tc_read_arcs(path, fmt, index_base)
+    t1 = time.perf_counter()
+    g = tc_graph_create(n, src, dst, device=device)
+    torch.cuda.synchronize(device)
+    t2 = time.perf_counter()
+    g.profile(True)
+    counts = tc_census(g)
+    t3 = time.perf_counter()
+    prof = g.profile_get()
+    g.close()
+    timing = {"read_graph": t1 - t0, "build_csr": t2 - t1, "build_csr_device": prof["build_ms"] / 1e3,
+              "plan": prof["plan_ms"] / 1e3, "census_kernels": prof["census_ms"] / 1e3,
+              "census_call": t3 - t2, "total": t3 - t0}
+    return counts, timing
