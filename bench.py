@@ -48,6 +48,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--config", default="C3")
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--mode", default="16", choices=["16", "64"],
+                   help="16-class isomorphic census (default) or the 64-type census (f1)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=15.0,
                    help="bounded oracle sample for cpu_baseline")
@@ -248,7 +250,10 @@ def run_ours(args):
         launches = g.launches()
         if profile:
             g.profile(True)
-        counts = tcb.tc_census_multi(g, comm, stream) if comm else tcb.tc_census(g, stream)
+        if args.mode == "64":
+            counts = tcb.tc_census64(g, stream)
+        else:
+            counts = tcb.tc_census_multi(g, comm, stream) if comm else tcb.tc_census(g, stream)
         launches += g.launches()
         prof = g.profile_get() if profile else None
         stats = g.stats()
@@ -327,6 +332,8 @@ def run_ours(args):
     bytes_alg = 4.0 * work + 24.0 * items      # 4(du+dv)+24 B per dyad
     achieved = bytes_alg / (avg_k[dom] * 1e-3) / 1e9
     names = ["k_census_thread", "k_census_warp"]
+    if args.mode == "64":
+        names = ["k_census_thread64", "k_census_warp64"]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
     if os.path.exists(tp):
@@ -345,6 +352,7 @@ def run_ours(args):
                 "l2": "inputs > L2 (arcs %.0f MB, sort keys %.0f MB) and a 512 MB L2 flush "
                       "before every timed step" % (8 * a.m / 1e6, 32 * a.m / 1e6),
                 "step": "a1 build from device arcs + a2 plan + a3/a4 kernels + a5 closing",
+                "census_mode": "64-type (f1)" if args.mode == "64" else "16-class",
                 "parallelism": "dp%d (replicated CSR, degree-balanced dyad shards, 1 NCCL "
                                "allreduce)" % world if world > 1 else "single GPU"}),
             "phases_ms": {"build": build_ms, "plan": plan_ms, "census_kernels": census_ms,

@@ -133,6 +133,17 @@ void tc_graph_destroy(tc_graph *g);
 tc_status tc_census(const tc_graph *g, void *cuda_stream, uint64_t counts[16],
                     uint64_t *c003_hi);
 
+/* 64-type (non-isomorphic) census, SURVEY.md section 8(f) f1 (P:258,
+ * P:327): counts[c] = triads whose TriadCode (bit weights of Fig.
+ * P:329-347) is c, in the labelling the B-M loop assigns -- a connected
+ * triad is coded at (u, v, w) with (u, v) its counting canonical dyad and w
+ * the canonical third vertex; a dyadic triad gets code pre =
+ * IsEdge(u,v) + 2 IsEdge(v,u) (reading 12); code 0 = C(n,3) -
+ * sum, low word in counts[0], high word in *c0_hi (same rules as c003_hi).
+ * Folding counts through the TriadTable gives tc_census.  Synchronous. */
+tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
+                      uint64_t *c0_hi);
+
 /* Partial census over canonical dyads [dyad_begin, dyad_end) (clamped to
  * [0, D)): classes 2..16 only, partial[0] = 0.  Partials over any partition
  * of [0, D) sum to the full census minus 003.  Synchronous. */

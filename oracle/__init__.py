@@ -68,6 +68,8 @@ def _load():
             lib.og_census.argtypes = [vp, u64p, u64p]
             lib.og_census_range.argtypes = [vp, u64, u64, u64p]
             lib.og_bruteforce.argtypes = [vp, u64p, u64p]
+            lib.og_census64.argtypes = [vp, u64p, u64p]
+            lib.og_bruteforce64.argtypes = [vp, u64p, u64p]
             lib.og_dyad_costs.argtypes = [vp, u64p]
             lib.og_choose3_u128.argtypes = [u64, u64p, u64p]
             lib.og_graph_n.restype = u64
@@ -148,6 +150,23 @@ class Graph:
         rc = self._lib.og_bruteforce(self._h, _p(c, ctypes.c_uint64), ctypes.byref(hi))
         if rc != 0:
             raise OracleError("og_bruteforce failed: %d" % rc)
+        out = [int(x) for x in c]
+        out[0] += int(hi.value) << 64
+        return out
+
+    def census64(self) -> list[int]:
+        """64-type (non-isomorphic) census in the B-M labelling."""
+        return self._c64(self._lib.og_census64, "og_census64")
+
+    def bruteforce64(self) -> list[int]:
+        return self._c64(self._lib.og_bruteforce64, "og_bruteforce64")
+
+    def _c64(self, fn, name):
+        c = np.zeros(64, np.uint64)
+        hi = ctypes.c_uint64(0)
+        rc = fn(self._h, _p(c, ctypes.c_uint64), ctypes.byref(hi))
+        if rc != 0:
+            raise OracleError("%s failed: %d" % (name, rc))
         out = [int(x) for x in c]
         out[0] += int(hi.value) << 64
         return out

@@ -28,6 +28,16 @@
  *                    partition sum to the full census.
  *   og_bruteforce    the naive O(n^3) census of P:261: every unordered triple
  *                    classified by the 6-probe TriadCode of Fig. P:329-347.
+ *   og_census64      the non-isomorphic (64-type) census of the same loop
+ *                    (TriadCode "returns this value + 1
+ *                    if main algorithm calculates non-isomorphic triad
+ *                    census"); dyadic triads go to code pre (DESIGN.md
+ *                    reading 12); code 0 closes as C(n,3) - sum.
+ *   og_bruteforce64  O(n^3) 64-type census in the labelling B-M uses: a
+ *                    connected triple a<b<c is coded at (u,v,w) = (a,b,c) if
+ *                    a,b are adjacent, else (a,c,b) (the canonical dyad that
+ *                    counts it); a dyadic triple at its one connected
+ *                    pair (x<y) with code pre(x,y); an empty triple at 0.
  *
  * Graph sanitising (reading 9): self-loops are dropped,
  * duplicate arcs are merged.  Vertex ids are 0-based, n is explicit.
@@ -298,7 +308,7 @@ static og_u128 og_choose3(uint64_t n)
  * into C[1..16] (1-based).  S is materialised exactly as line 8:
  * S <- N(u) U N(v) \ {u,v}.  Returns -1 on allocation failure. */
 static int og_census_core(const og_graph *g, const uint8_t T[64],
-                          uint64_t db, uint64_t de, uint64_t C[17])
+                          uint64_t db, uint64_t de, uint64_t *C, int mode64)
 {
     uint64_t n = g->n;
     uint64_t maxd = 0;
@@ -330,8 +340,8 @@ static int og_census_core(const og_graph *g, const uint8_t T[64],
             int e0 = og_is_edge(g, u, v);
             int e1 = og_is_edge(g, v, u);
             int pre = e0 + 2 * e1;
-            /* lines 9-14 */
-            int type = (e0 && e1) ? 3 : 2;
+            /* lines 9-14 (64-type mode: the dyadic triads' code is pre) */
+            int type = mode64 ? pre + 1 : ((e0 && e1) ? 3 : 2);
             C[type] += n - s - 2;
             /* lines 15-20 */
             for (uint64_t t = 0; t < s; t++) {
@@ -343,7 +353,7 @@ static int og_census_core(const og_graph *g, const uint8_t T[64],
                     code += 8 * og_is_edge(g, w, u);
                     code += 16 * og_is_edge(g, v, w);
                     code += 32 * og_is_edge(g, w, v);
-                    C[T[code]] += 1;                                        /* line 18 */
+                    C[mode64 ? code + 1 : T[code]] += 1;                    /* line 18 */
                 }
             }
         }
@@ -362,7 +372,7 @@ int og_census(const og_graph *g, uint64_t counts[16], uint64_t *c003_hi)
     if (g->n > 0xffffffffull) return -2;
     uint64_t C[17];
     memset(C, 0, sizeof(C));
-    if (og_census_core(g, T, 0, UINT64_MAX, C) != 0) return -1;
+    if (og_census_core(g, T, 0, UINT64_MAX, C, 0) != 0) return -1;
     /* lines 24-28: Census[1] <- n(n-1)(n-2)/6 - sum */
     og_u128 sum = 0;
     for (int i = 2; i <= 16; i++) sum += C[i];
@@ -382,9 +392,30 @@ int og_census_range(const og_graph *g, uint64_t db, uint64_t de, uint64_t counts
     if (og_triad_table(T) != 0) return -3;
     uint64_t C[17];
     memset(C, 0, sizeof(C));
-    if (og_census_core(g, T, db, de, C) != 0) return -1;
+    if (og_census_core(g, T, db, de, C, 0) != 0) return -1;
     counts[0] = 0;
     for (int i = 2; i <= 16; i++) counts[i - 1] = C[i];
+    return 0;
+}
+
+/* 64-type census: counts[c] = triads with TriadCode c (c = 0..63) in the
+ * B-M labelling; counts[0] low word, *c0_hi high word. */
+int og_census64(const og_graph *g, uint64_t counts[64], uint64_t *c0_hi)
+{
+    uint8_t T[64];
+    if (og_triad_table(T) != 0) return -3;
+    if (g->n > 0xffffffffull) return -2;
+    uint64_t C[65];
+    memset(C, 0, sizeof(C));
+    if (og_census_core(g, T, 0, UINT64_MAX, C, 1) != 0) return -1;
+    og_u128 sum = 0;
+    for (int i = 2; i <= 64; i++) sum += C[i];
+    og_u128 total = og_choose3(g->n);
+    if (sum > total) return -4;
+    og_u128 c0 = total - sum;
+    counts[0] = (uint64_t)c0;
+    *c0_hi = (uint64_t)(c0 >> 64);
+    for (int i = 2; i <= 64; i++) counts[i - 1] = C[i];
     return 0;
 }
 
@@ -440,6 +471,47 @@ int og_bruteforce(const og_graph *g, uint64_t counts[16], uint64_t *c003_hi)
     counts[0] = (uint64_t)C[1];
     *c003_hi = (uint64_t)(C[1] >> 64);
     for (int i = 2; i <= 16; i++) counts[i - 1] = (uint64_t)C[i];
+    return 0;
+}
+
+/* O(n^3) 64-type census in the B-M labelling (see header). */
+int og_bruteforce64(const og_graph *g, uint64_t counts[64], uint64_t *c0_hi)
+{
+    uint64_t n = g->n;
+    if (n > 20000) return -2;
+    uint64_t words = (n + 63) / 64;
+    uint64_t *adj = (uint64_t *)calloc((n && words) ? n * words : 1, sizeof(uint64_t));
+    if (!adj) return -1;
+    for (uint64_t u = 0; u < n; u++)
+        for (uint64_t i = g->e_off[u]; i < g->e_off[u + 1]; i++) {
+            uint64_t v = g->e_col[i];
+            adj[u * words + v / 64] |= 1ull << (v % 64);
+        }
+#define OG_ARC(a, b) ((int)((adj[(a) * words + (b) / 64] >> ((b) % 64)) & 1ull))
+#define OG_CODE(u, v, w) (OG_ARC(u, v) + 2 * OG_ARC(v, u) + 4 * OG_ARC(u, w) + 8 * OG_ARC(w, u) + \
+                          16 * OG_ARC(v, w) + 32 * OG_ARC(w, v))
+    og_u128 C[64];
+    for (int i = 0; i < 64; i++) C[i] = 0;
+    for (uint64_t a = 0; a < n; a++)
+        for (uint64_t b = a + 1; b < n; b++)
+            for (uint64_t c = b + 1; c < n; c++) {
+                int ab = OG_ARC(a, b) | OG_ARC(b, a);
+                int ac = OG_ARC(a, c) | OG_ARC(c, a);
+                int bc = OG_ARC(b, c) | OG_ARC(c, b);
+                int code;
+                if (ab + ac + bc >= 2) code = ab ? OG_CODE(a, b, c) : OG_CODE(a, c, b);
+                else if (ab) code = OG_CODE(a, b, c) & 3;
+                else if (ac) code = OG_CODE(a, c, b) & 3;
+                else if (bc) code = OG_CODE(b, c, a) & 3;
+                else code = 0;
+                C[code] += 1;
+            }
+#undef OG_CODE
+#undef OG_ARC
+    free(adj);
+    counts[0] = (uint64_t)C[0];
+    *c0_hi = (uint64_t)(C[0] >> 64);
+    for (int i = 1; i < 64; i++) counts[i] = (uint64_t)C[i];
     return 0;
 }
 

@@ -24,7 +24,7 @@ CLASS_NAMES = ("003", "012", "102", "021D", "021U", "021C", "111D", "111U",
                "030T", "030C", "201", "120D", "120U", "120C", "210", "300")
 
 __all__ = ["tc_read_arcs", "census_file", "CLASS_NAMES", "Graph", "TCError", "tc_graph_create", "tc_census", "tc_census_range",
-           "tc_census_enqueue", "tc_census_multi", "tc_close_census", "tc_shard_bounds",
+           "tc_census_enqueue", "tc_census_multi", "tc_census64", "tc_close_census", "tc_shard_bounds",
            "tc_shard_bounds_host", "tc_comm_create", "tc_comm_unique_id", "Comm",
            "census", "lib"]
 
@@ -155,6 +155,16 @@ def tc_census(g: Graph, stream=None) -> list[int]:
     hi = ctypes.c_uint64(0)
     check(lib.tc_census(g.handle, _stream_ptr(stream), c, ctypes.byref(hi)), "tc_census")
     return _join003(c, hi.value)
+
+
+def tc_census64(g: Graph, stream=None) -> list[int]:
+    """64-type (non-isomorphic) census in the B-M labelling; [0] exact."""
+    c = (ctypes.c_uint64 * 64)()
+    hi = ctypes.c_uint64(0)
+    check(lib.tc_census64(g.handle, _stream_ptr(stream), c, ctypes.byref(hi)), "tc_census64")
+    out = [int(x) for x in c]
+    out[0] += int(hi.value) << 64
+    return out
 
 
 def tc_census_range(g: Graph, begin: int, end: int, stream=None) -> list[int]:

@@ -55,6 +55,7 @@ _SIGS = {
     "tc_graph_destroy": (None, [vp]),
     "tc_census": (cint, [vp, vp, u64p, u64p]),
     "tc_census_range": (cint, [vp, u64, u64, vp, u64p]),
+    "tc_census64": (cint, [vp, vp, u64p, u64p]),
     "tc_census_enqueue": (cint, [vp, u64, u64, vp, vp]),
     "tc_close_census": (cint, [u64, u64p, u64p]),
     "tc_shard_bounds_host": (cint, [u64p, u64, cint, u64, u64p]),

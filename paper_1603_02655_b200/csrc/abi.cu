@@ -251,6 +251,45 @@ tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_
     return census_partial_sync(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, partial);
 }
 
+tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
+                      uint64_t *c0_hi) {
+    if (!g || !counts) {
+        set_error("NULL argument");
+        return TC_E_INVALID;
+    }
+    TC_CUDA(cudaSetDevice(g->device));
+    cudaStream_t s = (cudaStream_t)cuda_stream;
+    Mem mem = g->mem;
+    mem.stream = s;
+    DevBuf<uint64_t> d;
+    tc_status st = d.allocate(mem, 64);
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(d.p, 0, 64 * sizeof(uint64_t), s));
+    tc_graph *mg = const_cast<tc_graph *>(g);
+    mg->launches = 0;
+    st = census_range_device(g, 0, g->st.dyads, s, d.p, g->profile ? &mg->prof : nullptr,
+                             &mg->launches, 1);
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaMemcpyAsync(counts, d.p, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    unsigned __int128 sum = 0;
+    for (int k = 1; k < 64; k++) sum += counts[k];
+    unsigned __int128 total = choose3(g->st.n);
+    if (sum > total) {
+        set_error("64-type census sum exceeds C(n,3): internal inconsistency");
+        return TC_E_INVALID;
+    }
+    unsigned __int128 c0 = total - sum;
+    counts[0] = (uint64_t)c0;
+    const uint64_t hi = (uint64_t)(c0 >> 64);
+    if (c0_hi) *c0_hi = hi;
+    else if (hi) {
+        set_error("code 0 count needs a high word but c0_hi is NULL");
+        return TC_E_OVERFLOW;
+    }
+    return TC_OK;
+}
+
 tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint64_t kappa,
                                uint64_t *bounds) {
     if (!bounds || world < 1 || world > 1024 || (D && !cost)) {

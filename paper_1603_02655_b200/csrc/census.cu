@@ -280,10 +280,160 @@ k_census_warp(const BinItem4 *__restrict__ items, const unsigned long long *__re
     block_finish(c, wsh, d_counts);
 }
 
+// ---------------------------------------------------------------------------
+// 64-type (non-isomorphic) census: the same
+// merge, but every canonical trip counts its TriadCode itself (P:327, P:343:
+// "returns this value + 1 if main algorithm calculates non-isomorphic triad
+// census"), in a per-warp shared uint32 histogram of 64 codes (flushed to
+// per-warp uint64 totals before it can overflow); dyadic triads go to code
+// pre (reading 12).  Code 0 is closed on the host.
+// ---------------------------------------------------------------------------
+struct Acc64 {
+    uint64_t dy[3];          // dyadic triads of codes 1, 2, 3 (= pre)
+    uint32_t pending;        // trips since the last flush
+};
+
+__device__ __forceinline__ void merge_diag64(const uint32_t *__restrict__ adj, uint32_t oa,
+                                             uint32_t a, uint32_t ob, uint32_t b, uint32_t ku,
+                                             uint32_t kv, uint32_t pre, uint32_t d0, uint32_t d1,
+                                             uint32_t *hist, Acc64 &c) {
+    uint32_t i = 0;
+    if (d0 > 0) i = merge_path(adj + oa, a, adj + ob, b, d0);
+    uint32_t pa = oa + i, pb = ob + (d0 - i);
+    uint32_t lastA = i > 0 ? (__ldg(adj + pa - 1) | 3u) : 0u;
+    uint32_t x = __ldg(adj + pa), y = __ldg(adj + pb);
+    uint32_t I = 0;
+    for (uint32_t t = d0; t < d1; t++) {
+        const uint32_t kx = x | 3u, ky = y | 3u;
+        const bool ta = kx <= ky;
+        const bool tb = ky <= kx;
+        const uint32_t ca = ta ? ((x << 2) & 12u) : 0u;
+        const uint32_t cb = tb ? ((y << 4) & 48u) : 0u;
+        const bool canon = ta ? (kx > kv) : ((ky != lastA) & (ky > ku));
+        I += (uint32_t)(ta & tb);
+        if (canon) atomicAdd(&hist[pre | ca | cb], 1u);
+        lastA = ta ? kx : lastA;
+        pa += ta;
+        pb += !ta;
+        const uint32_t nv = __ldg(adj + (ta ? pa : pb));
+        x = ta ? nv : x;
+        y = ta ? y : nv;
+    }
+    c.dy[pre - 1] += I;
+}
+
+// flush the warp's uint32 histogram into its uint64 totals (all lanes active)
+__device__ __forceinline__ void warp_flush64(uint32_t *hist, unsigned long long *tot, Acc64 &c) {
+    __syncwarp();
+    const uint32_t lane = threadIdx.x & 31;
+    for (int k = lane; k < 64; k += 32) {
+        tot[k] += hist[k];
+        hist[k] = 0;
+    }
+    __syncwarp();
+    c.pending = 0;
+}
+
+__device__ __forceinline__ void warp_reserve64(uint32_t *hist, unsigned long long *tot, Acc64 &c,
+                                               uint32_t len) {
+    if (__any_sync(0xffffffffu, c.pending + len > (1u << 26))) warp_flush64(hist, tot, c);
+    c.pending += len;
+}
+
+struct Smem64 {
+    uint32_t hist[kWarps][64];
+    unsigned long long tot[kWarps][64];
+};
+
+__device__ __forceinline__ void block_setup64(Smem64 &S) {
+    for (int i = threadIdx.x; i < kWarps * 64; i += blockDim.x) {
+        (&S.hist[0][0])[i] = 0;
+        (&S.tot[0][0])[i] = 0;
+    }
+    __syncthreads();
+}
+
+__device__ __forceinline__ void block_finish64(Smem64 &S, Acc64 &c, unsigned long long *d_counts) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    warp_flush64(S.hist[warp], S.tot[warp], c);
+#pragma unroll
+    for (int q = 0; q < 3; q++) {
+        unsigned long long v = c.dy[q];
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) S.tot[warp][q + 1] += v;
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < 64; k += blockDim.x) {
+        if (k == 0) continue;
+        unsigned long long v = 0;
+        for (int w = 0; w < kWarps; w++) v += S.tot[w][k];
+        if (v) atomicAdd(&d_counts[k], v);
+    }
+}
+
+__global__ void __launch_bounds__(kCensusThreads)
+k_census_thread64(const BinItem2 *__restrict__ items, const uint32_t *__restrict__ tile_count,
+                  uint64_t ntiles, const uint32_t *__restrict__ off,
+                  const uint32_t *__restrict__ adj, uint64_t n, unsigned long long *d_counts) {
+    __shared__ Smem64 S;
+    block_setup64(S);
+    Acc64 c{{0, 0, 0}, 0};
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const uint32_t cnt = __ldg(tile_count + tile);
+        const BinItem2 *it = items + tile * kPlanTile;
+        for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
+            const bool valid = base + lane < cnt;
+            BinItem2 e{0, 0};
+            uint32_t ou = 0, a = 0, ov = 0, b = 0;
+            if (valid) {
+                e = it[base + lane];
+                row_of(off, e.u, ou, a);
+                row_of(off, e.e >> 2, ov, b);
+            }
+            warp_reserve64(S.hist[warp], S.tot[warp], c, a + b);
+            if (valid) {
+                const uint32_t pre = e.e & 3u;
+                c.dy[pre - 1] += n - a - b;
+                merge_diag64(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, 0, a + b,
+                             S.hist[warp], c);
+            }
+        }
+    }
+    block_finish64(S, c, d_counts);
+}
+
+__global__ void __launch_bounds__(kCensusThreads)
+k_census_warp64(const BinItem4 *__restrict__ items, const unsigned long long *__restrict__ d_count,
+                const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
+                unsigned long long *d_counts) {
+    __shared__ Smem64 S;
+    block_setup64(S);
+    Acc64 c{{0, 0, 0}, 0};
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t count = *d_count;
+    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t it = wid; it < count; it += nw) {
+        const BinItem4 e = items[it];
+        const uint32_t v = e.e >> 2, pre = e.e & 3u;
+        uint32_t ou, a, ov, b;
+        row_of(off, e.u, ou, a);
+        row_of(off, v, ov, b);
+        const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
+        const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
+        warp_reserve64(S.hist[warp], S.tot[warp], c, d1 - d0);
+        if (e.d0 == 0 && lane == 0) c.dy[pre - 1] += n - a - b;
+        if (d0 < d1)
+            merge_diag64(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, d0, d1, S.hist[warp], c);
+    }
+    block_finish64(S, c, d_counts);
+}
+
 }  // namespace
 
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
-                      cudaEvent_t *ev, uint64_t *launches) {
+                      cudaEvent_t *ev, uint64_t *launches, int mode64) {
     const uint64_t n = g->st.n;
     unsigned long long *out = reinterpret_cast<unsigned long long *>(d_counts);
     int sms = 148;
@@ -291,6 +441,17 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     const unsigned grid = (unsigned)sms * kCensusBlocksPerSM;
     const size_t dyn = 0;
     if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
+    if (mode64) {
+        k_census_thread64<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->off,
+                                                         g->adj, n, out);
+        TC_CUDA(cudaGetLastError());
+        if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
+        k_census_warp64<<<grid, kCensusThreads, 0, s>>>(bl.w, bl.w_count, g->off, g->adj, n, out);
+        TC_CUDA(cudaGetLastError());
+        if (ev) TC_CUDA(cudaEventRecord(ev[2], s));
+        *launches += 2;
+        return TC_OK;
+    }
     k_census_thread<<<grid, kCensusThreads, dyn, s>>>(bl.t, bl.t_count, bl.ntiles, g->off, g->adj,
                                                      n, out);
     TC_CUDA(cudaGetLastError());

@@ -22,7 +22,8 @@ constexpr unsigned kCensusBlocksPerSM = 8;
 
 
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]
+// (mode64: TriadCodes 1..63 into d_counts[1..63])
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
-                      cudaEvent_t *ev /* 3 events or null */, uint64_t *launches);
+                      cudaEvent_t *ev /* 3 events or null */, uint64_t *launches, int mode64);
 
 }  // namespace tc

@@ -147,7 +147,8 @@ __global__ void k_lower_bounds(const uint64_t *__restrict__ excl, uint64_t D,
 }  // namespace
 
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
-                              uint64_t *d_counts, tc_profile *prof, uint64_t *launches) {
+                              uint64_t *d_counts, tc_profile *prof, uint64_t *launches,
+                              int mode64) {
     const uint64_t D = g->st.dyads;
     if (k1 > D) k1 = D;
     if (k0 >= k1) return TC_OK;
@@ -188,7 +189,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     lists.ntiles = ntiles;
     lists.w = wl.p;
     lists.w_count = stats.p;
-    st = launch_bins(g, lists, s, d_counts, prof ? ev + 1 : nullptr, launches);
+    st = launch_bins(g, lists, s, d_counts, prof ? ev + 1 : nullptr, launches, mode64);
     if (st != TC_OK) return st;
     if (prof) {
         TC_CUDA(cudaEventRecord(ev[3], s));

@@ -109,7 +109,8 @@ namespace tc {
 tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, uint64_t m,
                     cudaStream_t s);                                  // a1, csr_build.cu
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
-                              uint64_t *d_counts, tc_profile *prof, uint64_t *launches);  // a2-a4
+                              uint64_t *d_counts, tc_profile *prof, uint64_t *launches,
+                              int mode64 = 0);  // a2-a4
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
                               uint64_t *bounds);                      // schedule.cu
 

@@ -209,3 +209,14 @@ def test_census_multi_world1_nccl(tcb):
     finally:
         comm.close()
         g.close()
+
+
+def test_census64_vs_oracle(tcb):
+    # f1: 64-type census, GPU vs oracle element by element
+    cases = [synth.random_digraph(n, p, seed=7000 + n, loops=True, dups=3)
+             for n, p in ((5, 0.5), (60, 0.1), (300, 0.05), (200, 0.6))]
+    cases += [synth.make_config("C1"), synth.make_config("C2"), synth.rmat(12, 16, seed=3)]
+    for a in cases:
+        g = tcb.tc_graph_create(a.n, a.src, a.dst)
+        assert tcb.tc_census64(g) == oracle.Graph(a.n, a.src, a.dst).census64(), a.meta
+        g.close()
