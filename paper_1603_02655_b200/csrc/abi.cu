@@ -29,9 +29,25 @@ tc_status cuda_status(cudaError_t e, const char *what) {
     return e == cudaErrorMemoryAllocation ? TC_E_OOM : TC_E_CUDA;
 }
 
+// default allocator: the device's CUDA memory pool, stream ordered, with
+// freed blocks kept for reuse (release threshold = unlimited), so repeated
+// builds and censuses do not return memory to the driver
+static void keep_default_pool() {
+    static thread_local int done_dev = -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev == done_dev) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    done_dev = dev;
+}
+
 void *Mem::alloc(size_t bytes) {
     if (bytes == 0) bytes = 1;
     if (custom) return hook.alloc(bytes, (void *)stream, hook.ctx);
+    keep_default_pool();
     void *p = nullptr;
     if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
         cudaGetLastError();

@@ -5,21 +5,29 @@
 // of P:458-469) where every entry carries the 2-bit direction code, so the
 // census never probes IsEdge / IsNeighbour -- the tags answer them.
 //
-//   1. emit      arc (s,d), s != d  ->  keys (s<<32 | d<<2 | 1) and
-//                (d<<32 | s<<2 | 2); self-loops -> all-ones sentinel keys
-//                that sort last (strict digraph); range check.
-//   2. sort      LSD radix sort on the column bits then the row bits.
-//   3. compact   head = first key of a (row, col) run.  A ballot/popc
-//                compaction (count pass, scan of tile counts, write pass)
-//                numbers the heads (entry index r) and the canonical heads
-//                row < col (dyad index k, canonical order P:277-281); each
-//                head ORs its run's tags (dedup, mutual merge) and writes
-//                adj[r + row] = col<<2 | tag, the dyad list and, at row
-//                boundaries, the row offsets.  Every row ends with one
-//                sentinel entry 0xffffffff (greater than any real entry), so
-//                the census merge runs off a row end without bounds checks:
-//                row u = adj[off[u], off[u+1] - 1), |N(u)| = off[u+1]-off[u]-1.
-//   4. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost.
+//   1. emit      arc (s,d), s != d -> one canonical key (min<<32 | max<<2 |
+//                dir), dir = 1 if min->max else 2; self-loops -> all-ones
+//                sentinel keys that sort last (strict digraph);
+//                range check.
+//   2. sort      LSD radix sort (radix_sort.cu) on the max bits, then the
+//                min bits: canonical pairs in the algorithm's own dyad order
+//                (u ascending, v ascending).
+//   3. compact   a ballot/popc compaction keeps the first key of each (min,
+//                max) run with the OR of the run's direction bits (dedup +
+//                mutual merge): the canonical dyad list dyad_u / dyad_e (the
+//                upper halves of the rows) and the transposed keys (max<<32 |
+//                min<<2 | swapped tag), the lower halves.
+//   4. sort      stable LSD sort of the D transposed keys on the row bits
+//                only (they arrive sorted by min, so each row ends up sorted).
+//   5. assemble  row u = lower part (w < u) then upper part (w > u), both
+//                already sorted, then one sentinel 0xffffffff (greater than
+//                any real entry) so the census merge runs off a row end
+//                without bounds checks:  row u = adj[off[u], off[u+1] - 1),
+//                off[u] = lo_start[u] + up_start[u] + u.
+//   6. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost.
+// Sorting one key per arc and D transposed keys (instead of both
+// orientations of every arc) cuts the sort work by a quarter and halves the
+// compaction.
 #include <stdio.h>
 
 #include "radix_sort.cuh"
@@ -41,79 +49,76 @@ __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restr
     unsigned long long loops = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t s = src[i], d = dst[i];
-        ulonglong2 kv;
+        const uint32_t s = src[i], d = dst[i];
+        uint64_t k;
         if (s >= n || d >= n) {
             atomicMin(&scratch[0], (unsigned long long)i);
-            kv = make_ulonglong2(kSentinel, kSentinel);
+            k = kSentinel;
         } else if (s == d) {
             loops++;
-            kv = make_ulonglong2(kSentinel, kSentinel);
+            k = kSentinel;
         } else {
-            kv = make_ulonglong2(((uint64_t)s << 32) | ((uint64_t)d << 2) | 1ull,
-                                 ((uint64_t)d << 32) | ((uint64_t)s << 2) | 2ull);
+            const uint32_t lo = s < d ? s : d, hi = s < d ? d : s;
+            k = ((uint64_t)lo << 32) | ((uint64_t)hi << 2) | (s < d ? 1ull : 2ull);
         }
-        reinterpret_cast<ulonglong2 *>(keys)[i] = kv;
+        keys[i] = k;
     }
     for (int o = 16; o; o >>= 1) loops += __shfl_xor_sync(0xffffffffu, loops, o);
     if ((threadIdx.x & 31) == 0 && loops) atomicAdd(&scratch[1], loops);
 }
 
-// (row, col) of a sorted key; heads: first key of each (row, col) run
 __device__ __forceinline__ uint32_t key_row(uint64_t k) { return (uint32_t)(k >> 32); }
 __device__ __forceinline__ uint32_t key_col(uint64_t k) { return (uint32_t)((k >> 2) & 0x3fffffffu); }
+__device__ __forceinline__ uint32_t swap_tag(uint32_t t) { return ((t & 1u) << 1) | (t >> 1); }
 
-// flags of key i (warp-striped: lanes hold consecutive keys)
-__device__ __forceinline__ void head_flags(const uint64_t *__restrict__ key, size_t L, size_t i,
-                                           uint64_t &k, uint64_t &prev, bool &head, bool &canon) {
+// key i (warp-striped: lanes hold consecutive keys), its predecessor, and
+// whether it starts a (row, col) run
+__device__ __forceinline__ void run_head(const uint64_t *__restrict__ key, size_t L, size_t i,
+                                         uint64_t &k, uint64_t &prev, bool &head) {
     const uint32_t lane = threadIdx.x & 31;
     k = i < L ? __ldg(key + i) : kSentinel;
     prev = __shfl_up_sync(0xffffffffu, k, 1);
     if (lane == 0) prev = (i > 0 && i - 1 < L) ? __ldg(key + i - 1) : kSentinel;
     head = i < L && (i == 0 || (prev >> 2) != (k >> 2));
-    canon = head && key_row(k) < key_col(k);
 }
 
-// pass 1: per warp (512 keys), number of heads | canonical heads << 32
+// pass 1: per warp (512 keys), number of run heads
 __global__ void __launch_bounds__(kHcThreads)
-k_head_count(const uint64_t *__restrict__ key, size_t L, uint64_t *__restrict__ warp_tot) {
+k_head_count(const uint64_t *__restrict__ key, size_t L, uint32_t *__restrict__ warp_tot) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
-    uint32_t nh = 0, nc = 0;
+    uint32_t nh = 0;
 #pragma unroll 4
     for (int r = 0; r < kHcItems; r++) {
         uint64_t k, prev;
-        bool head, canon;
-        head_flags(key, L, base + (size_t)r * 32 + lane, k, prev, head, canon);
+        bool head;
+        run_head(key, L, base + (size_t)r * 32 + lane, k, prev, head);
         nh += __popc(__ballot_sync(0xffffffffu, head));
-        nc += __popc(__ballot_sync(0xffffffffu, canon));
     }
-    if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = (uint64_t)nh | ((uint64_t)nc << 32);
+    if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = nh;
 }
 
-// pass 2: write adj / dyad lists / row offsets at the compacted positions
-// (warp_off = exclusive scan of pass 1's per-warp totals)
+// pass 2: canonical dyad list, transposed keys and up_start at row changes
+// (warp_off = exclusive scan of pass 1's per-warp counts)
 __global__ void __launch_bounds__(kHcThreads)
-k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restrict__ warp_off,
-             uint32_t *__restrict__ adj, uint32_t *__restrict__ du, uint32_t *__restrict__ de,
-             uint32_t *__restrict__ off) {
+k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restrict__ warp_off,
+             uint32_t *__restrict__ du, uint32_t *__restrict__ de, uint64_t *__restrict__ tk,
+             uint32_t *__restrict__ up_start) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
-    const uint64_t woff = warp_off[(size_t)blockIdx.x * kHcWarps + warp];
-    uint32_t r0 = (uint32_t)woff, k0 = (uint32_t)(woff >> 32);
+    uint32_t k0 = warp_off[(size_t)blockIdx.x * kHcWarps + warp];
     for (int r = 0; r < kHcItems; r++) {
         const size_t i = base + (size_t)r * 32 + lane;
         uint64_t k, prev;
-        bool head, canon;
-        head_flags(key, L, i, k, prev, head, canon);
+        bool head;
+        run_head(key, L, i, k, prev, head);
         const uint32_t bh = __ballot_sync(0xffffffffu, head);
-        const uint32_t bc = __ballot_sync(0xffffffffu, canon);
         // next key (lane + 1, or a load for lane 31) for the run's tag OR
         uint64_t nxt = __shfl_down_sync(0xffffffffu, k, 1);
         if (lane == 31) nxt = i + 1 < L ? __ldg(key + i + 1) : kSentinel;
         if (head) {
-            const uint32_t rr = r0 + __popc(bh & lt);
+            const uint32_t kk = k0 + __popc(bh & lt);
             const uint32_t row = key_row(k), col = key_col(k);
             uint32_t tag = (uint32_t)(k & 3u);
             if ((nxt >> 2) == (k >> 2)) {            // mutual pair and/or duplicates
@@ -125,37 +130,78 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint64_t *__restr
                     tag |= (uint32_t)(kj & 3u);
                 }
             }
-            const uint32_t e = (col << 2) | tag;
-            adj[rr + row] = e;
-            if (canon) {
-                const uint32_t kk = k0 + __popc(bc & lt);
-                du[kk] = row;
-                de[kk] = e;
-            }
-            // first entry of row `row`: rows (prev_row, row] start here
-            if (i == 0 || key_row(prev) != row) {
-                off[row] = rr + row;
+            du[kk] = row;
+            de[kk] = (col << 2) | tag;
+            tk[kk] = ((uint64_t)col << 32) | ((uint64_t)row << 2) | swap_tag(tag);
+            if (i == 0 || key_row(prev) != row) {     // rows (prev_row, row] start here
                 const uint32_t first = i == 0 ? 0u : key_row(prev) + 1;
 #pragma unroll 1
-                for (uint32_t x = first; x < row; x++) off[x] = rr + x;   // empty rows
+                for (uint32_t x = first; x <= row; x++) up_start[x] = kk;
             }
         }
-        r0 += __popc(bh);
-        k0 += __popc(bc);
+        k0 += __popc(bh);
     }
 }
 
-__global__ void k_fill_tail(uint32_t *off, uint64_t from, uint64_t n, uint32_t nnz) {
-    for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
-         x += (uint64_t)gridDim.x * blockDim.x)
-        off[x] = nnz + (uint32_t)x;
+// start[x] = first index of row x in a row-sorted key array (rows with no
+// keys get the next row's start); the tail (rows after the last) is filled
+// by k_fill_tail
+__global__ void k_row_starts(const uint64_t *__restrict__ key, size_t L, uint32_t *start) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t row = key_row(__ldg(key + i));
+        const uint32_t prev = i ? key_row(__ldg(key + i - 1)) : 0xffffffffu;
+        if (i == 0 || prev != row) {
+            const uint32_t first = i == 0 ? 0u : prev + 1;
+            for (uint32_t x = first; x <= row; x++) start[x] = (uint32_t)i;
+        }
+    }
 }
 
-// row terminators (and slack entries past the last row for look-ahead loads)
-__global__ void k_sentinels(const uint32_t *__restrict__ off, uint64_t n, uint32_t *adj) {
-    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n + 8;
+__global__ void k_fill_tail(uint32_t *start, uint64_t from, uint64_t n, uint32_t val) {
+    for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
          x += (uint64_t)gridDim.x * blockDim.x)
-        adj[x < n ? off[x + 1] - 1 : off[n] + (x - n)] = 0xffffffffu;
+        start[x] = val;
+}
+
+// lower entries: row r's i-th key of the row-sorted transposed list goes to
+// off[r] + (i - lo_start[r]) = up_start[r] + r + i
+__global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
+                              const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < D;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const uint64_t k = __ldg(tk + i);
+        const uint32_t r = key_row(k);
+        adj[__ldg(up_start + r) + r + (uint32_t)i] = (uint32_t)k;
+    }
+}
+
+// upper entries: dyad k of row u goes to off[u] + lo_cnt[u] + (k - up_start[u])
+// = lo_start[u + 1] + u + k
+__global__ void k_write_upper(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
+                              size_t D, const uint32_t *__restrict__ lo_start,
+                              uint32_t *__restrict__ adj) {
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < D;
+         k += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t u = __ldg(du + k);
+        adj[__ldg(lo_start + u + 1) + u + (uint32_t)k] = __ldg(de + k);
+    }
+}
+
+// off[u] = lo_start[u] + up_start[u] + u; sentinel at off[u+1] - 1; slack after
+__global__ void k_offsets(const uint32_t *__restrict__ lo_start,
+                          const uint32_t *__restrict__ up_start, uint64_t n,
+                          uint32_t *__restrict__ off, uint32_t *__restrict__ adj) {
+    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n + 8;
+         u += (uint64_t)gridDim.x * blockDim.x) {
+        if (u <= n) {
+            const uint32_t o = lo_start[u] + up_start[u] + (uint32_t)u;
+            off[u] = o;
+            if (u > 0) adj[o - 1] = 0xffffffffu;    // terminator of row u - 1
+        } else {
+            adj[lo_start[n] + up_start[n] + (uint32_t)u - 1] = 0xffffffffu;   // slack
+        }
+    }
 }
 
 __device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
@@ -222,15 +268,13 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     Mem &mem = g->mem;
 
     DevBuf<unsigned long long> scratch;
-    if ((st = scratch.allocate(mem, 16)) != TC_OK) return st;
-    unsigned long long init[16] = {~0ull, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    if ((st = scratch.allocate(mem, 8)) != TC_OK) return st;
+    unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
     TC_CUDA(cudaMemcpyAsync(scratch.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
 
-    size_t L0 = 2 * (size_t)m;
     DevBuf<uint64_t> keys, tmp;
-    if ((st = keys.allocate(mem, L0)) != TC_OK) return st;
-    if ((st = tmp.allocate(mem, L0)) != TC_OK) return st;
-
+    if ((st = keys.allocate(mem, m)) != TC_OK) return st;
+    if ((st = tmp.allocate(mem, m)) != TC_OK) return st;
     if (m) {
         k_emit<<<grid_for(m, 256), 256, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
         g->launches++;
@@ -244,67 +288,103 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         return TC_E_RANGE;
     }
     const uint64_t loops = h[1];
-    const size_t L = L0 - 2 * loops;
-    if ((uint64_t)L + n + 8 >= (1ull << 32)) {
+    const size_t L = m - loops;                     // canonical keys before dedup
+    if (2ull * L + n + 8 >= (1ull << 32)) {
         set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
-                  (unsigned long long)(L + n));
+                  (unsigned long long)(2 * L + n));
         return TC_E_INVALID;
     }
 
-    // 2. sort by (row, col): column bits first, then row bits
+    // 2. sort canonical keys by (min, max): max bits first, then min bits
     int b = 1;
     while (b < 32 && (1ull << b) < n) b++;
     RadixPass passes[16];
     int np = radix_passes_for(2, b, passes);
     np += radix_passes_for(32, b, passes + np);
     uint64_t *sorted = keys.p;
-    if ((st = radix_sort_u64(mem, keys.p, tmp.p, L0, passes, np, s, &g->launches, &sorted)) !=
+    if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted)) !=
         TC_OK)
         return st;
+    uint64_t *spare = sorted == keys.p ? tmp.p : keys.p;
 
-    // 3. compaction -> adj, dyad list, offsets
-    size_t cap = L ? L : 1;
-    uint32_t *adj = (uint32_t *)mem.alloc((L + n + 8) * sizeof(uint32_t));
-    uint32_t *du = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
-    uint32_t *de = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
-    uint32_t *dc = (uint32_t *)mem.alloc((cap / 2 + 1) * sizeof(uint32_t));
+    // 3. compaction -> canonical dyads (upper halves) + transposed keys
+    const size_t cap = L ? L : 1;
+    uint32_t *du = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
+    uint32_t *de = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
+    uint32_t *dc = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *off = (uint32_t *)mem.alloc((n + 1) * sizeof(uint32_t));
-    g->adj = adj; g->adj_n = L + n + 8;
-    g->dyad_u = du; g->dyad_n = cap / 2 + 1;
+    g->dyad_u = du; g->dyad_n = cap;
     g->dyad_e = de;
     g->dyad_c = dc;
     g->off = off; g->off_n = n + 1;
-    if (!adj || !du || !de || !dc || !off) {
+    DevBuf<uint32_t> up_start, lo_start;
+    if (!du || !de || !dc || !off) {
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
-    uint64_t tot = 0, lastkey = 0;
+    if ((st = up_start.allocate(mem, n + 1)) != TC_OK) return st;
+    if ((st = lo_start.allocate(mem, n + 1)) != TC_OK) return st;
+    uint32_t D = 0;
+    uint64_t lastkey = 0;
     if (L) {
         const size_t ntiles = (L + kHcTile - 1) / kHcTile;
-        DevBuf<uint64_t> tt, total;
-        if ((st = tt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
+        DevBuf<uint32_t> wt, total;
+        if ((st = wt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
         if ((st = total.allocate(mem, 1)) != TC_OK) return st;
-        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p);
+        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p);
         TC_CUDA(cudaGetLastError());
-        st = scan_exclusive<uint64_t>(mem, ntiles * kHcWarps, ArrayIn<uint64_t>{tt.p},
-                                      ArrayOutExcl<uint64_t>{tt.p}, total.p, s, &g->launches);
+        st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
+                                      ArrayOutExcl<uint32_t>{wt.p}, total.p, s, &g->launches);
         if (st != TC_OK) return st;
-        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, tt.p, adj, du, de, off);
+        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p, du, de, spare,
+                                                             up_start.p);
         TC_CUDA(cudaGetLastError());
         g->launches += 2;
-        TC_CUDA(cudaMemcpyAsync(&tot, total.p, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaMemcpyAsync(&lastkey, sorted + (L - 1), sizeof(uint64_t),
                                 cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
     }
-    const uint64_t nnz = tot & 0xffffffffull, D = tot >> 32;
-    uint64_t from = L ? ((lastkey >> 32) + 1) : 0;
-    k_fill_tail<<<grid_for(n + 1 - from, 256), 256, 0, s>>>(off, from, n, (uint32_t)nnz);
-    k_sentinels<<<grid_for(n + 8, 256), 256, 0, s>>>(off, n, adj);
-    g->launches += 2;
+    // rows after the last canonical row have no upper entries
+    const uint64_t up_from = D ? ((lastkey >> 32) + 1) : 0;
+    k_fill_tail<<<grid_for(n + 1 - up_from, 256), 256, 0, s>>>(up_start.p, up_from, n, D);
     TC_CUDA(cudaGetLastError());
 
-    // 4. stats
+    // 4. lower halves: stable sort of the transposed keys on the row bits
+    uint64_t *tsorted = spare;
+    RadixPass rpasses[8];
+    const int nrp = radix_passes_for(32, b, rpasses);
+    uint64_t *tother = spare == keys.p ? tmp.p : keys.p;
+    if ((st = radix_sort_u64(mem, spare, tother, D, rpasses, nrp, s, &g->launches, &tsorted)) !=
+        TC_OK)
+        return st;
+    uint64_t tlast = 0;
+    if (D) {
+        k_row_starts<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, lo_start.p);
+        TC_CUDA(cudaMemcpyAsync(&tlast, tsorted + (D - 1), sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+    }
+    const uint64_t lo_from = D ? ((tlast >> 32) + 1) : 0;
+    k_fill_tail<<<grid_for(n + 1 - lo_from, 256), 256, 0, s>>>(lo_start.p, lo_from, n, D);
+
+    // 5. assemble the symmetric rows
+    const uint64_t nnz = 2ull * D;
+    uint32_t *adj = (uint32_t *)mem.alloc((nnz + n + 8) * sizeof(uint32_t));
+    g->adj = adj; g->adj_n = nnz + n + 8;
+    if (!adj) {
+        set_error("device allocation for the CSR failed");
+        return TC_E_OOM;
+    }
+    if (D) {
+        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj);
+        k_write_upper<<<grid_for(D, 256), 256, 0, s>>>(du, de, D, lo_start.p, adj);
+    }
+    k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, adj);
+    g->launches += D ? 6 : 3;
+    TC_CUDA(cudaGetLastError());
+
+    // 6. stats
     k_vertex_stats<<<grid_for(n, 256), 256, 0, s>>>(off, n, scratch.p + 4);
     if (D) k_dyad_cost_stats<<<grid_for(D, 256), 256, 0, s>>>(off, du, de, D, dc, scratch.p + 4);
     g->launches += D ? 2 : 1;
@@ -319,11 +399,6 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     g->st.m = h[6];
     g->st.mutual_dyads = h[7];
     g->st.dups_dropped = m - loops - h[6];
-    if (nnz != 2 * D) {
-        set_error("internal: CSR has %llu entries for %llu dyads", (unsigned long long)nnz,
-                  (unsigned long long)D);
-        return TC_E_CUDA;
-    }
     return TC_OK;
 }
 

@@ -11,7 +11,7 @@ s = torch.from_numpy(a.src.view('int32')).cuda()
 d = torch.from_numpy(a.dst.view('int32')).cuda()
 for rep in range(4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
-    g = tcb.tc_graph_create(a.n, s, d)
+    g = tcb.tc_graph_create(a.n, s, d, use_torch_allocator=os.environ.get("TC_TORCH_ALLOC", "1") == "1")
     torch.cuda.synchronize(); t1 = time.perf_counter()
     g.profile(True)
     c = g.census()
