@@ -146,7 +146,13 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
 
 /* Partial census over canonical dyads [dyad_begin, dyad_end) (clamped to
  * [0, D)): classes 2..16 only, partial[0] = 0.  Partials over any partition
- * of [0, D) sum to the full census minus 003.  Synchronous. */
+ * of [0, D) sum to the full census minus 003.  Classes 4..16
+ * (021D..300) are exactly those of the range's canonical triads.
+ * Classes 2..3 (012, 102): each dyad (u,v) of the range contributes
+ * n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}| to its class, plus one
+ * to the class of dyad (v,x) for every x > v in N(u) & N(v) -- the
+ * intersection element u of that later dyad, which its own merge (starting
+ * at entries > v) does not see (reading 14).  Synchronous. */
 tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                           void *cuda_stream, uint64_t partial[16]);
 

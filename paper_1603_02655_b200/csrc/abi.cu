@@ -194,6 +194,9 @@ void tc_graph_destroy(tc_graph *g) {
     g->mem.free(g->dyad_u, g->dyad_n * 4);
     g->mem.free(g->dyad_e, g->dyad_n * 4);
     g->mem.free(g->dyad_c, g->dyad_n * 4);
+    g->mem.free(g->dyad_pb, g->dyad_n * 4);
+    g->mem.free(g->dyad_t, g->dyad_n * 4);
+    g->mem.free(g->ups, g->ups_n * 4);
     cudaStreamSynchronize(g->stream);
     delete g;
 }

@@ -8,32 +8,42 @@
 //     A / B (0 if absent): exactly IsEdge(u,w)+2*IsEdge(w,u) and
 //     IsEdge(v,w)+2*IsEdge(w,v) of Fig. TriadCode;
 //   * line 16's predicate  v < w or (u < w < v and not IsNeighbour(u,w))
-//     is, for w from A (tu != 0): w > v, and for w only in B (tu == 0):
-//     w > u; both reject w = u and w = v;
+//     never holds for w <= u, so the merge starts at the first entry w > u
+//     of both rows (ups[u] in row u, dyad_pb in row v; csr_build.cu).  Then
+//     the predicate is, for w from A (tu != 0): w > v, and for w only in B
+//     (tu == 0): always (w > u by construction);
 //   * code = pre | tu<<2 | tv<<4 (bit weights 1,2,4,8,16,32 of P:329-347) and
-//     class = TriadTable[code], looked up in shared memory (64 bytes:
-//     every lookup is conflict free);
+//     class = TriadTable[code], looked up in shared memory;
 //   * the dyadic term n - |S| - 2 of line 14, with |S| = |N(u)|+|N(v)|-I-2
-//     (I = |N(u) & N(v)|), is added as (n - du - dv) once per dyad plus one
-//     per intersection element, to class 3 (pre == 3, mutual) or class 2.
+//     (I = |N(u) & N(v)|), is  n - du - dv  (added by the plan, schedule.cu)
+//     plus one per element of I.  Elements w > u of I are met by this merge.
+//     An element x < u of I is the smallest vertex of a triangle x < u < v;
+//     it is met, instead, by the merge of dyad (x, u) as its canonical
+//     intersection element v > u -- so every canonical intersection element
+//     w > v of dyad (u, v) also adds the dyadic triad (v, w, u-excluded)
+//     owed to dyad (v, w): one to class 102 if tv == 3 (v <-> w mutual),
+//     else to class 012 (reading 14).  Each triangle's three
+//     intersections are thus counted exactly once, and the census is the
+//     paper's; only the split of 012/102 between dyad ranges moves.
 //
 // Merge-path form: trip t consumes exactly one list element (A first on
-// equal ids), so a dyad of cost c = du + dv is exactly c trips; an
-// intersection element is classified when its A copy is consumed (both tags
-// are visible then) and its B twin is skipped.  A thread, a lane or a chunk
-// processes any diagonal range [d0, d1) after a merge-path split of d0.
-// Rows end in a sentinel (csr_build.cu), so the loop has no bounds checks,
-// the next element of each list is loaded one consumption ahead, and the
-// thread bin prefetches both rows into L2 when a dyad starts.
-// Thread-bin warps hold dyads of identical cost, so every lane runs the same
-// trip count (no divergence); warp items split one dyad over 32 lanes.
+// equal ids), so a dyad of merge length t (entries > u of both rows) is
+// exactly t trips; an intersection element is classified when its A copy is
+// consumed (both tags are visible then) and its B twin is skipped.  A thread
+// or a lane processes any diagonal range [d0, d1) after a merge-path split
+// of d0.  Rows end in a sentinel (csr_build.cu), so the loop has no bounds
+// checks, the next element of each list is loaded one consumption ahead, and
+// the thread bin prefetches both rows into L2 when a dyad starts.
+// Thread-bin warps hold dyads of identical merge length, so every lane runs
+// the same trip count (no divergence); warp items split one dyad over 32
+// lanes.
 //
-// a4: per thread, one uint64 of 16 4-bit class counters (+1 per trip at
-// nibble 4*class; non-canonical trips hit the unused nibble of class 003),
-// spilled every <= 15 trips into two uint64 of 8-bit counters (even / odd
-// classes), which a warp flushes (REDUX sum per class) into per-warp shared
-// totals before they can overflow; blocks end with one global atomicAdd per
-// class.
+// a4: per thread, one uint64 of 16 4-bit class counters; a canonical trip
+// adds the 64-bit increment table[code] (one nibble for its class, plus one
+// for the dyadic correction above), spilled every <= 15 trips into two
+// uint64 of 8-bit counters (even / odd classes), which a warp flushes (REDUX
+// sum per class) into per-warp shared totals before they can overflow;
+// blocks end with one global atomicAdd per class.
 #include "census.cuh"
 
 namespace tc {
@@ -74,19 +84,19 @@ __device__ __forceinline__ void spill(Acc &c) {
     c.n4 = 0;
 }
 
-__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
-    uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+__device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
+    uint64_t v;
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(addr));
     return v;
 }
 
-// Warp-level flush (all 32 lanes active): each connected class (3..15) is
-// summed over the warp with one REDUX and lane 0 adds it to the warp's own
-// shared slots (plain adds; 64-bit shared atomics are CAS loops on sm_100).
+// Warp-level flush (all 32 lanes active): each class 1..15 is summed over
+// the warp with one REDUX and lane 0 adds it to the warp's own shared slots
+// (plain adds; 64-bit shared atomics are CAS loops on sm_100).
 __device__ __forceinline__ void warp_flush(Acc &c, unsigned long long *wsh) {
     const uint32_t lane = threadIdx.x & 31;
 #pragma unroll
-    for (int k = 3; k < 16; k++) {
+    for (int k = 1; k < 16; k++) {
         uint32_t x = (uint32_t)(((k & 1) ? c.od8 : c.ev8) >> (8 * (k >> 1))) & 255u;
         uint32_t s = __reduce_add_sync(0xffffffffu, x);
         if (lane == 0) wsh[k] += s;
@@ -115,14 +125,15 @@ __device__ __forceinline__ uint32_t merge_path(const uint32_t *__restrict__ A, u
     return lo;
 }
 
-// Classify merge diagonals [d0, d1) of dyad (u, v).  A = adj[oa, oa+a),
-// B = adj[ob, ob+b), both followed by a sentinel; ku = u<<2|3, kv = v<<2|3;
-// tab = shared address of the 64-entry nibble-shift table.  The caller has
+// Classify merge diagonals [d0, d1) of dyad (u, v).  A = adj[oa, oa+a) (the
+// entries w > u of N(u)), B = adj[ob, ob+b) (the entries w > u of N(v)),
+// both followed by more of their row and a sentinel; kv = v<<2|3; tab =
+// shared address of the 64-entry uint64 increment table.  The caller has
 // reserved d1 - d0 byte-counter increments (warp_reserve).
 __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uint32_t oa,
-                                           uint32_t a, uint32_t ob, uint32_t b, uint32_t ku,
-                                           uint32_t kv, uint32_t pre, uint32_t d0, uint32_t d1,
-                                           uint32_t tab, Acc &c) {
+                                           uint32_t a, uint32_t ob, uint32_t b, uint32_t kv,
+                                           uint32_t pre, uint32_t d0, uint32_t d1, uint32_t tab,
+                                           Acc &c) {
     uint32_t i = 0;
     if (d0 > 0) i = merge_path(adj + oa, a, adj + ob, b, d0);
     uint32_t pa = oa + i, pb = ob + (d0 - i);
@@ -131,7 +142,7 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
     uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
     uint32_t I = 0;
-    const uint32_t tabp = tab + pre;
+    const uint32_t tabp = tab + 8u * pre;
     uint32_t t = d0;
     while (t < d1) {
         const uint32_t lim = min(d1, t + 15u);   // nibble counters hold 15
@@ -139,15 +150,14 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
             const uint32_t kx = x | 3u, ky = y | 3u;
             const bool ta = kx <= ky;            // consume A (ties: A first)
             const bool tb = ky <= kx;            // B's id is the merged id
-            // code - pre = tu<<2 | tv<<4 with tu = tag in A, tv = tag in B
-            const uint32_t ca = ta ? ((x << 2) & 12u) : 0u;
-            const uint32_t cb = tb ? ((y << 4) & 48u) : 0u;
-            // A element: w > v.  B-only element: w > u, and not the B twin of
-            // the A element just consumed (already classified with both tags).
-            const bool canon = ta ? (kx > kv) : ((ky != lastA) & (ky > ku));
+            // 8 * (code - pre) = tu<<5 | tv<<7, tu = tag in A, tv = tag in B
+            const uint32_t ca = ta ? ((x << 5) & 0x60u) : 0u;
+            const uint32_t cb = tb ? ((y << 7) & 0x180u) : 0u;
+            // A element: w > v.  B-only element: canonical unless it is the
+            // B twin of the A element just consumed (classified already).
+            const bool canon = ta ? (kx > kv) : (ky != lastA);
             I += (uint32_t)(ta & tb);
-            const uint32_t sh = canon ? lds_u8(tabp + (ca | cb)) : 0u;
-            c.n4 += 1ull << sh;
+            c.n4 += canon ? lds_u64(tabp + (ca | cb)) : 0ull;
             lastA = ta ? kx : lastA;
             pa += ta;
             pb += !ta;
@@ -162,9 +172,17 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     add_dyadic(c, pre, I);
 }
 
-// shared table: code -> 4 * class (nibble shift); wsh[warp][16]: per-warp totals
-__device__ __forceinline__ void block_setup(uint8_t *tab, unsigned long long (*wsh)[16]) {
-    if (threadIdx.x < 64) tab[threadIdx.x] = (uint8_t)(4u * c_triad_table[threadIdx.x]);
+// shared increment table: code -> one nibble at 4 * class, plus (both tags
+// set: a canonical intersection element w > v) one nibble at class 102 if
+// tv == 3 else 012, the dyadic triad owed to dyad (v, w); per-warp totals
+__device__ __forceinline__ void block_setup(unsigned long long *tab,
+                                            unsigned long long (*wsh)[16]) {
+    if (threadIdx.x < 64) {
+        const uint32_t code = threadIdx.x, tu = (code >> 2) & 3u, tv = code >> 4;
+        unsigned long long inc = 1ull << (4u * c_triad_table[code]);
+        if (tu && tv) inc += 1ull << (tv == 3u ? 8u : 4u);
+        tab[code] = inc;
+    }
     for (int i = threadIdx.x; i < kWarps * 16; i += blockDim.x) (&wsh[0][0])[i] = 0;
     __syncthreads();
 }
@@ -201,22 +219,30 @@ __device__ __forceinline__ void prefetch_row_l2(const uint32_t *adj, uint32_t o,
         asm volatile("prefetch.global.L2 [%0];" ::"l"(q));
 }
 
-// row u of the sentinel-padded CSR: start and |N(u)|
-__device__ __forceinline__ void row_of(const uint32_t *__restrict__ off, uint32_t u,
-                                       uint32_t &o, uint32_t &len) {
-    o = __ldg(off + u);
-    len = __ldg(off + u + 1) - o - 1u;
+// merge of a warp-bin dyad k: starts and lengths of A and B
+struct WarpDyad {
+    uint32_t oa, a, ob, b, e;
+};
+__device__ __forceinline__ WarpDyad warp_dyad(const BinLists &L, const uint32_t *__restrict__ off,
+                                              const uint32_t *__restrict__ ups, uint32_t k) {
+    WarpDyad w;
+    const uint32_t u = __ldg(L.du + k);
+    w.e = __ldg(L.de + k);
+    w.oa = __ldg(ups + u);
+    w.a = __ldg(off + u + 1) - 1u - w.oa;
+    w.ob = __ldg(L.dpb + k);
+    w.b = __ldg(off + (w.e >> 2) + 1) - 1u - w.ob;
+    return w;
 }
 
 // thread bin: one thread per dyad.  Block-persistent over tiles of
 // kPlanTile consecutive canonical dyads; inside a tile the plan ordered the
-// thread-bin dyads by cost, so each warp's lanes run equal trip counts while
-// the tile keeps the N(u) rows of nearby u hot in L1/L2.
+// thread-bin dyads by merge length, so each warp's lanes run equal trip
+// counts while the tile keeps the N(u) rows of nearby u hot in L1/L2.
 __global__ void __launch_bounds__(kCensusThreads)
-k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__ tile_count,
-                uint64_t ntiles, const uint32_t *__restrict__ off,
-                const uint32_t *__restrict__ adj, uint64_t n, unsigned long long *d_counts) {
-    __shared__ uint8_t tab_s[64];
+k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
+                uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
+    __shared__ unsigned long long tab_s[64];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
@@ -225,24 +251,19 @@ k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t cnt = __ldg(tile_count + tile);
-        const BinItem2 *it = items + tile * kPlanTile;
+        const BinItemT *it = items + tile * kPlanTile;
         for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
-            BinItem2 e{0, 0};
-            uint32_t ou = 0, a = 0, ov = 0, b = 0;
+            BinItemT e{0, 0, 0, 0};
             if (valid) {
                 e = it[base + lane];
-                row_of(off, e.u, ou, a);
-                row_of(off, e.e >> 2, ov, b);
-                prefetch_row_l2(adj, ou, a);
-                prefetch_row_l2(adj, ov, b);
+                // the two parts are <= t entries each (their lengths are not
+                // in the item; the whole-diagonal merge needs no split)
+                prefetch_row_l2(adj, e.pa, e.t);
+                prefetch_row_l2(adj, e.pb, e.t);
             }
-            warp_reserve(c, wsh[warp], a + b);
-            if (valid) {
-                const uint32_t pre = e.e & 3u;
-                add_dyadic(c, pre, n - a - b);
-                merge_diag(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, 0, a + b, tab, c);
-            }
+            warp_reserve(c, wsh[warp], e.t);
+            if (valid) merge_diag(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
         }
     }
     block_finish(c, wsh, d_counts);
@@ -251,31 +272,25 @@ k_census_thread(const BinItem2 *__restrict__ items, const uint32_t *__restrict__
 // warp bin: one warp per item = one dyad's diagonals [d0, d1), 32 lane
 // segments of <= kLaneSpan diagonals each
 __global__ void __launch_bounds__(kCensusThreads)
-k_census_warp(const BinItem4 *__restrict__ items, const unsigned long long *__restrict__ d_count,
-              const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
-              unsigned long long *d_counts) {
-    __shared__ uint8_t tab_s[64];
+k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
+              const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
+    __shared__ unsigned long long tab_s[64];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t count = *d_count;
+    const uint64_t count = *L.w_count;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t it = wid; it < count; it += nw) {
-        const BinItem4 e = items[it];
-        const uint32_t v = e.e >> 2, pre = e.e & 3u;
-        uint32_t ou, a, ov, b;
-        row_of(off, e.u, ou, a);
-        row_of(off, v, ov, b);
+        const BinItemW e = L.w[it];
+        const WarpDyad w = warp_dyad(L, off, ups, e.k);
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
         const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
         warp_reserve(c, wsh[warp], d1 - d0);
-        if (e.d0 == 0 && lane == 0) add_dyadic(c, pre, n - a - b);
-        if (d0 < d1)
-            merge_diag(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, d0, d1, tab, c);
+        if (d0 < d1) merge_diag(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
     }
     block_finish(c, wsh, d_counts);
 }
@@ -286,7 +301,8 @@ k_census_warp(const BinItem4 *__restrict__ items, const unsigned long long *__re
 // "returns this value + 1 if main algorithm calculates non-isomorphic triad
 // census"), in a per-warp shared uint32 histogram of 64 codes (flushed to
 // per-warp uint64 totals before it can overflow); dyadic triads go to code
-// pre (reading 12).  Code 0 is closed on the host.
+// pre (reading 12), the owed triad of a canonical intersection to
+// code tv.  Code 0 is closed on the host.
 // ---------------------------------------------------------------------------
 struct Acc64 {
     uint64_t dy[3];          // dyadic triads of codes 1, 2, 3 (= pre)
@@ -294,8 +310,8 @@ struct Acc64 {
 };
 
 __device__ __forceinline__ void merge_diag64(const uint32_t *__restrict__ adj, uint32_t oa,
-                                             uint32_t a, uint32_t ob, uint32_t b, uint32_t ku,
-                                             uint32_t kv, uint32_t pre, uint32_t d0, uint32_t d1,
+                                             uint32_t a, uint32_t ob, uint32_t b, uint32_t kv,
+                                             uint32_t pre, uint32_t d0, uint32_t d1,
                                              uint32_t *hist, Acc64 &c) {
     uint32_t i = 0;
     if (d0 > 0) i = merge_path(adj + oa, a, adj + ob, b, d0);
@@ -309,9 +325,12 @@ __device__ __forceinline__ void merge_diag64(const uint32_t *__restrict__ adj, u
         const bool tb = ky <= kx;
         const uint32_t ca = ta ? ((x << 2) & 12u) : 0u;
         const uint32_t cb = tb ? ((y << 4) & 48u) : 0u;
-        const bool canon = ta ? (kx > kv) : ((ky != lastA) & (ky > ku));
+        const bool canon = ta ? (kx > kv) : (ky != lastA);
         I += (uint32_t)(ta & tb);
-        if (canon) atomicAdd(&hist[pre | ca | cb], 1u);
+        if (canon) {
+            atomicAdd(&hist[pre | ca | cb], 1u);
+            if (ta & tb) atomicAdd(&hist[y & 3u], 1u);   // owed to dyad (v, w)
+        }
         lastA = ta ? kx : lastA;
         pa += ta;
         pb += !ta;
@@ -334,6 +353,8 @@ __device__ __forceinline__ void warp_flush64(uint32_t *hist, unsigned long long 
     c.pending = 0;
 }
 
+// a trip adds at most 1 to any code (its own code is >= 4, the owed dyadic
+// code is 1..3)
 __device__ __forceinline__ void warp_reserve64(uint32_t *hist, unsigned long long *tot, Acc64 &c,
                                                uint32_t len) {
     if (__any_sync(0xffffffffu, c.pending + len > (1u << 26))) warp_flush64(hist, tot, c);
@@ -372,60 +393,46 @@ __device__ __forceinline__ void block_finish64(Smem64 &S, Acc64 &c, unsigned lon
 }
 
 __global__ void __launch_bounds__(kCensusThreads)
-k_census_thread64(const BinItem2 *__restrict__ items, const uint32_t *__restrict__ tile_count,
-                  uint64_t ntiles, const uint32_t *__restrict__ off,
-                  const uint32_t *__restrict__ adj, uint64_t n, unsigned long long *d_counts) {
+k_census_thread64(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
+                  uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
     __shared__ Smem64 S;
     block_setup64(S);
     Acc64 c{{0, 0, 0}, 0};
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const uint32_t cnt = __ldg(tile_count + tile);
-        const BinItem2 *it = items + tile * kPlanTile;
+        const BinItemT *it = items + tile * kPlanTile;
         for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
-            BinItem2 e{0, 0};
-            uint32_t ou = 0, a = 0, ov = 0, b = 0;
-            if (valid) {
-                e = it[base + lane];
-                row_of(off, e.u, ou, a);
-                row_of(off, e.e >> 2, ov, b);
-            }
-            warp_reserve64(S.hist[warp], S.tot[warp], c, a + b);
-            if (valid) {
-                const uint32_t pre = e.e & 3u;
-                c.dy[pre - 1] += n - a - b;
-                merge_diag64(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, 0, a + b,
-                             S.hist[warp], c);
-            }
+            BinItemT e{0, 0, 0, 0};
+            if (valid) e = it[base + lane];
+            warp_reserve64(S.hist[warp], S.tot[warp], c, e.t);
+            if (valid)
+                merge_diag64(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, S.hist[warp], c);
         }
     }
     block_finish64(S, c, d_counts);
 }
 
 __global__ void __launch_bounds__(kCensusThreads)
-k_census_warp64(const BinItem4 *__restrict__ items, const unsigned long long *__restrict__ d_count,
-                const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj, uint64_t n,
+k_census_warp64(const BinLists L, const uint32_t *__restrict__ off,
+                const uint32_t *__restrict__ ups, const uint32_t *__restrict__ adj,
                 unsigned long long *d_counts) {
     __shared__ Smem64 S;
     block_setup64(S);
     Acc64 c{{0, 0, 0}, 0};
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint64_t count = *d_count;
+    const uint64_t count = *L.w_count;
     const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     for (uint64_t it = wid; it < count; it += nw) {
-        const BinItem4 e = items[it];
-        const uint32_t v = e.e >> 2, pre = e.e & 3u;
-        uint32_t ou, a, ov, b;
-        row_of(off, e.u, ou, a);
-        row_of(off, v, ov, b);
+        const BinItemW e = L.w[it];
+        const WarpDyad w = warp_dyad(L, off, ups, e.k);
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
         const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
         warp_reserve64(S.hist[warp], S.tot[warp], c, d1 - d0);
-        if (e.d0 == 0 && lane == 0) c.dy[pre - 1] += n - a - b;
         if (d0 < d1)
-            merge_diag64(adj, ou, a, ov, b, (e.u << 2) | 3u, e.e | 3u, pre, d0, d1, S.hist[warp], c);
+            merge_diag64(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, S.hist[warp], c);
     }
     block_finish64(S, c, d_counts);
 }
@@ -434,29 +441,22 @@ k_census_warp64(const BinItem4 *__restrict__ items, const unsigned long long *__
 
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
                       cudaEvent_t *ev, uint64_t *launches, int mode64) {
-    const uint64_t n = g->st.n;
     unsigned long long *out = reinterpret_cast<unsigned long long *>(d_counts);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
     const unsigned grid = (unsigned)sms * kCensusBlocksPerSM;
-    const size_t dyn = 0;
     if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
-    if (mode64) {
-        k_census_thread64<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->off,
-                                                         g->adj, n, out);
-        TC_CUDA(cudaGetLastError());
-        if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
-        k_census_warp64<<<grid, kCensusThreads, 0, s>>>(bl.w, bl.w_count, g->off, g->adj, n, out);
-        TC_CUDA(cudaGetLastError());
-        if (ev) TC_CUDA(cudaEventRecord(ev[2], s));
-        *launches += 2;
-        return TC_OK;
-    }
-    k_census_thread<<<grid, kCensusThreads, dyn, s>>>(bl.t, bl.t_count, bl.ntiles, g->off, g->adj,
-                                                     n, out);
+    if (mode64)
+        k_census_thread64<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->adj,
+                                                         out);
+    else
+        k_census_thread<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->adj, out);
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
-    k_census_warp<<<grid, kCensusThreads, 0, s>>>(bl.w, bl.w_count, g->off, g->adj, n, out);
+    if (mode64)
+        k_census_warp64<<<grid, kCensusThreads, 0, s>>>(bl, g->off, g->ups, g->adj, out);
+    else
+        k_census_warp<<<grid, kCensusThreads, 0, s>>>(bl, g->off, g->ups, g->adj, out);
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[2], s));
     *launches += 2;

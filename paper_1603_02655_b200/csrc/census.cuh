@@ -7,11 +7,12 @@ namespace tc {
 // item counts stay on the device (the kernels read them), so planning and
 // the census need no host round trip.
 struct BinLists {
-    const BinItem2 *t = nullptr;            // thread bin: tile-local lists sorted by cost
+    const BinItemT *t = nullptr;            // thread bin: tile-local lists sorted by length
     const uint32_t *t_count = nullptr;      // device: thread-bin items per tile
     uint64_t ntiles = 0;                    // tiles of kPlanTile canonical dyads
-    const BinItem4 *w = nullptr;            // warp bin: <= kWarpChunk diagonals per item
+    const BinItemW *w = nullptr;            // warp bin: <= kWarpChunk diagonals per item
     const unsigned long long *w_count = nullptr;   // device: number of warp-bin items
+    const uint32_t *du = nullptr, *de = nullptr, *dpb = nullptr;   // dyad arrays of the range
 };
 
 constexpr int kCensusThreads = 256;

@@ -15,16 +15,20 @@
 //   3. compact   a ballot/popc compaction keeps the first key of each (min,
 //                max) run with the OR of the run's direction bits (dedup +
 //                mutual merge): the canonical dyad list dyad_u / dyad_e (the
-//                upper halves of the rows) and the transposed keys (max<<32 |
-//                min<<2 | swapped tag), the lower halves.
+//                upper halves of the rows), the transposed keys (max<<32 |
+//                dyad index) and the lower entries (min<<2 | swapped tag).
 //   4. sort      stable LSD sort of the D transposed keys on the row bits
 //                only (they arrive sorted by min, so each row ends up sorted).
 //   5. assemble  row u = lower part (w < u) then upper part (w > u), both
 //                already sorted, then one sentinel 0xffffffff (greater than
 //                any real entry) so the census merge runs off a row end
 //                without bounds checks:  row u = adj[off[u], off[u+1] - 1),
-//                off[u] = lo_start[u] + up_start[u] + u.
-//   6. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost.
+//                off[u] = lo_start[u] + up_start[u] + u; ups[u] = start of
+//                the upper part of row u.
+//   6. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost c,
+//                where the entries w > u of row v start (dyad_pb: one past
+//                the lower entry u of row v) and the merge length t
+//                (census.cu).
 // Sorting one key per arc and D transposed keys (instead of both
 // orientations of every arc) cuts the sort work by a quarter and halves the
 // compaction.
@@ -98,12 +102,13 @@ k_head_count(const uint64_t *__restrict__ key, size_t L, uint32_t *__restrict__ 
     if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = nh;
 }
 
-// pass 2: canonical dyad list, transposed keys and up_start at row changes
-// (warp_off = exclusive scan of pass 1's per-warp counts)
+// pass 2: canonical dyad list, transposed keys (row v, dyad index k), the
+// lower entry of each dyad (ul[k] = u<<2 | swapped tag) and up_start at row
+// changes (warp_off = exclusive scan of pass 1's per-warp counts)
 __global__ void __launch_bounds__(kHcThreads)
 k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restrict__ warp_off,
              uint32_t *__restrict__ du, uint32_t *__restrict__ de, uint64_t *__restrict__ tk,
-             uint32_t *__restrict__ up_start) {
+             uint32_t *__restrict__ ul, uint32_t *__restrict__ up_start) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
@@ -132,7 +137,8 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restr
             }
             du[kk] = row;
             de[kk] = (col << 2) | tag;
-            tk[kk] = ((uint64_t)col << 32) | ((uint64_t)row << 2) | swap_tag(tag);
+            tk[kk] = ((uint64_t)col << 32) | kk;
+            ul[kk] = (row << 2) | swap_tag(tag);
             if (i == 0 || key_row(prev) != row) {     // rows (prev_row, row] start here
                 const uint32_t first = i == 0 ? 0u : key_row(prev) + 1;
 #pragma unroll 1
@@ -164,40 +170,38 @@ __global__ void k_fill_tail(uint32_t *start, uint64_t from, uint64_t n, uint32_t
         start[x] = val;
 }
 
-// lower entries: row r's i-th key of the row-sorted transposed list goes to
-// off[r] + (i - lo_start[r]) = up_start[r] + r + i
+// lower entries: row r's i-th key of the row-sorted transposed list is dyad
+// k = (u, r); its entry ul[k] goes to off[r] + (i - lo_start[r]) =
+// up_start[r] + r + i, and ul[k] is overwritten with that position + 1 (the
+// first entry w > u of row r: dyad_pb).  One random read-modify-write per
+// dyad into a D-word array (L2-resident at the Patents size) instead of a
+// search of row r.
 __global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
-                              const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj) {
+                              const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
+                              uint32_t *__restrict__ ul) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < D;
          i += (size_t)gridDim.x * blockDim.x) {
-        const uint64_t k = __ldg(tk + i);
-        const uint32_t r = key_row(k);
-        adj[__ldg(up_start + r) + r + (uint32_t)i] = (uint32_t)k;
+        const uint64_t key = __ldg(tk + i);
+        const uint32_t r = key_row(key), k = (uint32_t)key;
+        const uint32_t pos = __ldg(up_start + r) + r + (uint32_t)i;
+        adj[pos] = ul[k];
+        ul[k] = pos + 1u;
     }
 }
 
-// upper entries: dyad k of row u goes to off[u] + lo_cnt[u] + (k - up_start[u])
-// = lo_start[u + 1] + u + k
-__global__ void k_write_upper(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
-                              size_t D, const uint32_t *__restrict__ lo_start,
-                              uint32_t *__restrict__ adj) {
-    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < D;
-         k += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t u = __ldg(du + k);
-        adj[__ldg(lo_start + u + 1) + u + (uint32_t)k] = __ldg(de + k);
-    }
-}
-
-// off[u] = lo_start[u] + up_start[u] + u; sentinel at off[u+1] - 1; slack after
+// off[u] = lo_start[u] + up_start[u] + u; sentinel at off[u+1] - 1; slack
+// after; ups[u] = off[u] + |lower part of u| = first entry w > u of row u
 __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
                           const uint32_t *__restrict__ up_start, uint64_t n,
-                          uint32_t *__restrict__ off, uint32_t *__restrict__ adj) {
+                          uint32_t *__restrict__ off, uint32_t *__restrict__ ups,
+                          uint32_t *__restrict__ adj) {
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n + 8;
          u += (uint64_t)gridDim.x * blockDim.x) {
         if (u <= n) {
             const uint32_t o = lo_start[u] + up_start[u] + (uint32_t)u;
             off[u] = o;
             if (u > 0) adj[o - 1] = 0xffffffffu;    // terminator of row u - 1
+            if (u < n) ups[u] = lo_start[u + 1] + up_start[u] + (uint32_t)u;
         } else {
             adj[lo_start[n] + up_start[n] + (uint32_t)u - 1] = 0xffffffffu;   // slack
         }
@@ -230,17 +234,26 @@ __global__ void k_vertex_stats(const uint32_t *__restrict__ off, uint64_t n,
     }
 }
 
-// per canonical dyad: cost c = |N(u)| + |N(v)| (uniform workload);
+// upper entries + per-dyad data, one thread per canonical dyad k = (u, v):
+// the entry of v goes to ups[u] + (k - up_start[u]) = lo_start[u+1] + u + k;
+// cost c = |N(u)| + |N(v)| (uniform workload); merge length
+// t = |{w in N(u): w > u}| + |{w in N(v): w > u}| (dpb from k_write_lower);
 // stats [2] = distinct arcs m, [3] = mutual dyads
-__global__ void k_dyad_cost_stats(const uint32_t *__restrict__ off,
-                                  const uint32_t *__restrict__ du,
-                                  const uint32_t *__restrict__ de, uint64_t D,
-                                  uint32_t *__restrict__ dc, unsigned long long *out) {
+__global__ void k_write_upper(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
+                              const uint32_t *__restrict__ lo_start,
+                              const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
+                              const uint32_t *__restrict__ dpb, uint64_t D,
+                              uint32_t *__restrict__ adj, uint32_t *__restrict__ dc,
+                              uint32_t *__restrict__ dt, unsigned long long *out) {
     unsigned long long m = 0, mu = 0;
     for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < D;
          k += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t u = du[k], e = de[k], v = e >> 2, t = e & 3u;
-        dc[k] = (__ldg(off + u + 1) - __ldg(off + u)) + (__ldg(off + v + 1) - __ldg(off + v)) - 2;
+        const uint32_t u = du[k], e = de[k], v = e >> 2, t = e & 3u;
+        adj[__ldg(lo_start + u + 1) + u + (uint32_t)k] = e;
+        const uint32_t ou = __ldg(off + u), ou1 = __ldg(off + u + 1);
+        const uint32_t ov = __ldg(off + v), ov1 = __ldg(off + v + 1);
+        dc[k] = (ou1 - ou) + (ov1 - ov) - 2;
+        dt[k] = (ou1 - 1 - __ldg(ups + u)) + (ov1 - 1 - dpb[k]);
         m += __popc(t);
         mu += (t == 3u);
     }
@@ -312,13 +325,19 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     uint32_t *du = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *de = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *dc = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
+    uint32_t *dpb = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
+    uint32_t *dt = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *off = (uint32_t *)mem.alloc((n + 1) * sizeof(uint32_t));
+    uint32_t *ups = (uint32_t *)mem.alloc((n ? n : 1) * sizeof(uint32_t));
     g->dyad_u = du; g->dyad_n = cap;
     g->dyad_e = de;
     g->dyad_c = dc;
+    g->dyad_pb = dpb;
+    g->dyad_t = dt;
     g->off = off; g->off_n = n + 1;
+    g->ups = ups; g->ups_n = n ? n : 1;
     DevBuf<uint32_t> up_start, lo_start;
-    if (!du || !de || !dc || !off) {
+    if (!du || !de || !dc || !dpb || !dt || !off || !ups) {
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
@@ -336,7 +355,7 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
                                       ArrayOutExcl<uint32_t>{wt.p}, total.p, s, &g->launches);
         if (st != TC_OK) return st;
-        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p, du, de, spare,
+        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p, du, de, spare, dpb,
                                                              up_start.p);
         TC_CUDA(cudaGetLastError());
         g->launches += 2;
@@ -376,18 +395,18 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
+    k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj);
     if (D) {
-        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj);
-        k_write_upper<<<grid_for(D, 256), 256, 0, s>>>(du, de, D, lo_start.p, adj);
+        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj, dpb);
+        k_write_upper<<<grid_for(D, 256), 256, 0, s>>>(off, ups, lo_start.p, du, de, dpb, D, adj,
+                                                       dc, dt, scratch.p + 4);
     }
-    k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, adj);
-    g->launches += D ? 6 : 3;
+    g->launches += D ? 3 : 1;
     TC_CUDA(cudaGetLastError());
 
-    // 6. stats
+    // 6. vertex stats
     k_vertex_stats<<<grid_for(n, 256), 256, 0, s>>>(off, n, scratch.p + 4);
-    if (D) k_dyad_cost_stats<<<grid_for(D, 256), 256, 0, s>>>(off, du, de, D, dc, scratch.p + 4);
-    g->launches += D ? 2 : 1;
+    g->launches += 1;
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));

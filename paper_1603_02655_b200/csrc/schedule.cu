@@ -2,14 +2,16 @@
 //
 // Each canonical dyad (u, v), u < v, carries the paper's uniform workload
 // estimate c = |N(u)| + |N(v)| (Fig. P:1678-1705, "NsetSize + |N[u]| + |N[v]|
-// - 2"; the constant -2 changes no bin and no cut), computed
-// once by the CSR builder (dyad_c).  The plan is one stable counting sort of
-// the dyad range by c (256 digits: c itself for c <= kThreadBinMax, 255 for
-// every larger dyad):
-//   thread bin  c <= 254    items (u, e) ordered by c, so each warp holds
-//                           dyads of equal cost and its lanes run equal trip
-//                           counts (c merge diagonals each)
-//   warp bin    c > 254     the dyad is cut into warp items of <= 8160
+// - 2"; the constant -2 changes no bin and no cut) and its
+// exact merge length t = |{w in N(u): w > u}| + |{w in N(v): w > u}| (the
+// part of both rows the census merge walks, census.cu), both computed once
+// by the CSR builder (dyad_c, dyad_t).  The plan is one stable counting sort
+// of the dyad range by t (256 digits: t itself for t <= kThreadBinMax, 255
+// for every larger dyad):
+//   thread bin  t <= 254    items (row starts, e, lengths) ordered by t, so
+//                           each warp holds dyads of equal length and its
+//                           lanes run equal trip counts
+//   warp bin    t > 254     the dyad is cut into warp items of <= 8160
 //                           diagonals (32 lanes x <= 255), so power-law hubs
 //                           spread over many warps and never serialise one
 // All counts stay on the device: no host synchronisation in the census.
@@ -31,17 +33,24 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t c) {
 }
 
 // One block per tile of kPlanTile consecutive canonical dyads: a stable
-// tile-local counting sort of the thread-bin dyads by cost c (warp-level
-// ballot ranking, then a block scan over the 255 cost digits), so
-// the census keeps the tile's row locality and still gives every warp equal
-// trip counts.  Dyads with c > kThreadBinMax become warp items (<= 8160
-// diagonals each) appended through an atomic cursor.
+// tile-local counting sort of the thread-bin dyads by merge length t
+// (warp-level ballot ranking, then a block scan over the 255 length digits),
+// so the census keeps the tile's row locality and still gives every warp
+// equal trip counts.  Dyads with t > kThreadBinMax become warp items (<= 8160
+// diagonals each) appended through one atomic cursor per warp.  The plan
+// also adds every dyad's dyadic term n - |N(u)| - |N(v)| (the
+// census kernels add the intersection part) to d_counts, by class
+// (mode16: 012 / 102) or by code pre (mode64).
 // stats: [0] warp items, [1] thread-bin work, [2] warp-bin work, [3] big dyads
+struct PlanIn {
+    const uint32_t *du, *de, *dc, *dt, *dpb, *ups, *off;
+};
+
 __global__ void __launch_bounds__(kPlanThreads)
-k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
-            const uint32_t *__restrict__ dc, uint64_t N, BinItem2 *__restrict__ tl,
-            uint32_t *__restrict__ tile_count, BinItem4 *__restrict__ wl,
-            unsigned long long *__restrict__ stats) {
+k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
+            uint32_t *__restrict__ tile_count, BinItemW *__restrict__ wl,
+            unsigned long long *__restrict__ stats, unsigned long long *__restrict__ d_counts,
+            int mode64) {
     __shared__ uint32_t wc[kPlanWarps][kDigits];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kPlanWarps * kDigits; i += kPlanThreads) (&wc[0][0])[i] = 0;
@@ -54,7 +63,7 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
     for (int k = 0; k < kPlanItems; k++) {
         uint64_t i = tile0 + wbase + k * 32 + lane;
         bool valid = i < N;
-        cst[k] = valid ? __ldg(dc + i) : 0u;
+        cst[k] = valid ? __ldg(P.dt + i) : 0u;
         uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
         // lanes holding the same digit: one ballot per digit bit
         uint32_t peers = __ballot_sync(0xffffffffu, valid);
@@ -71,13 +80,13 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
         rank[k] = r;
     }
     __syncthreads();
+    uint32_t all;   // thread-bin dyads of the tile
     {   // thread d owns digit d: tile-local offsets (digit-major, then warp)
         const int d = threadIdx.x;
         uint32_t tot = 0;
 #pragma unroll
         for (int w = 0; w < kPlanWarps; w++) tot += wc[w][d];
         if (d == 255) tot = 0;      // big dyads are not in the thread list
-        uint32_t all;
         uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
         if (d == 0) tile_count[blockIdx.x] = all;
 #pragma unroll
@@ -88,38 +97,70 @@ k_plan_tile(const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
         }
     }
     __syncthreads();
-    BinItem2 *out = tl + tile0;
-    unsigned long long wt = 0, ww = 0, nbig = 0;
-#pragma unroll
+    extern __shared__ uint4 stage[];   // the tile's thread list, staged for coalesced stores
+    unsigned long long wt = 0, ww = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
+#pragma unroll 4
     for (int k = 0; k < kPlanItems; k++) {
-        uint64_t i = tile0 + wbase + k * 32 + lane;
-        if (i >= N) continue;
-        uint32_t c = cst[k], d = digit_of(c);
-        uint32_t u = __ldg(du + i), e = __ldg(de + i);
-        if (d < 255u) {
-            out[wc[warp][d] + rank[k]] = BinItem2{u, e};
-            wt += c;
-        } else {
-            uint32_t nch = (c + kWarpChunk - 1) / kWarpChunk;
-            unsigned long long at = atomicAdd(&stats[0], (unsigned long long)nch);
-            for (uint32_t q = 0; q < nch; q++) {
-                uint32_t d0 = q * kWarpChunk;
-                wl[at + q] = BinItem4{u, e, d0, min(c, d0 + kWarpChunk)};
+        const uint64_t i = tile0 + wbase + k * 32 + lane;
+        const bool valid = i < N;
+        const uint32_t c = cst[k], d = digit_of(c);
+        uint32_t nch = 0;
+        if (valid) {
+            const uint32_t u = __ldg(P.du + i), e = __ldg(P.de + i), pre = e & 3u;
+            const unsigned long long dy = n - __ldg(P.dc + i);
+            dy1 += pre == 1u ? dy : 0ull;
+            dy2 += pre == 2u ? dy : 0ull;
+            dy3 += pre == 3u ? dy : 0ull;
+            if (d < 255u) {
+                stage[wc[warp][d] + rank[k]] = make_uint4(__ldg(P.ups + u), __ldg(P.dpb + i), e, c);
+                wt += c;
+            } else {
+                nch = (c + kWarpChunk - 1) / kWarpChunk;
+                ww += c;
+                nbig++;
             }
-            ww += c;
-            nbig++;
+        }
+        // warp-aggregated cursor for the warp items
+        uint32_t incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        if (wtot) {
+            unsigned long long at = 0;
+            if (lane == 31) at = atomicAdd(&stats[0], (unsigned long long)wtot);
+            at = __shfl_sync(0xffffffffu, at, 31) + (incl - nch);
+            for (uint32_t q = 0; q < nch; q++) {
+                const uint32_t d0 = q * kWarpChunk;
+                wl[at + q] = BinItemW{(uint32_t)i, d0, min(c, d0 + kWarpChunk), 0u};
+            }
         }
     }
+    __syncthreads();
+    uint4 *out = reinterpret_cast<uint4 *>(tl + tile0);
+    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) out[j] = stage[j];
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         wt += __shfl_xor_sync(0xffffffffu, wt, o);
         ww += __shfl_xor_sync(0xffffffffu, ww, o);
         nbig += __shfl_xor_sync(0xffffffffu, nbig, o);
+        dy1 += __shfl_xor_sync(0xffffffffu, dy1, o);
+        dy2 += __shfl_xor_sync(0xffffffffu, dy2, o);
+        dy3 += __shfl_xor_sync(0xffffffffu, dy3, o);
     }
     if (lane == 0) {
         if (wt) atomicAdd(&stats[1], wt);
         if (ww) atomicAdd(&stats[2], ww);
         if (nbig) atomicAdd(&stats[3], nbig);
+        if (mode64) {
+            if (dy1) atomicAdd(&d_counts[1], dy1);
+            if (dy2) atomicAdd(&d_counts[2], dy2);
+        } else if (dy1 + dy2) {
+            atomicAdd(&d_counts[1], dy1 + dy2);
+        }
+        if (dy3) atomicAdd(&d_counts[mode64 ? 3 : 2], dy3);
     }
 }
 
@@ -166,21 +207,26 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     }
     tc_status st;
     const uint64_t ntiles = (N + kPlanTile - 1) / kPlanTile;
-    // upper bound on warp items: sum over big dyads of ceil(c / chunk)
+    // upper bound on warp items: sum over big dyads of ceil(t / chunk), t <= c
     const uint64_t nbig_max = g->st.sum_deg_sq / (kThreadBinMax + 1) + 1;
     const uint64_t wcap = (nbig_max < N ? nbig_max : N) + g->st.sum_deg_sq / kWarpChunk + 2;
     DevBuf<uint32_t> tcount;
-    DevBuf<BinItem2> tl;
-    DevBuf<BinItem4> wl;
+    DevBuf<BinItemT> tl;
+    DevBuf<BinItemW> wl;
     DevBuf<unsigned long long> stats;
     if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
     if ((st = stats.allocate(mem, 4)) != TC_OK) return st;
     TC_CUDA(cudaMemsetAsync(stats.p, 0, 4 * sizeof(unsigned long long), s));
-    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(g->dyad_u + k0, g->dyad_e + k0,
-                                                          g->dyad_c + k0, N, tl.p, tcount.p,
-                                                          wl.p, stats.p);
+    const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
+                   g->dyad_pb + k0, g->ups, g->off};
+    const int stage_bytes = kPlanTile * (int)sizeof(BinItemT);
+    TC_CUDA(cudaFuncSetAttribute(k_plan_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 stage_bytes));
+    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, stage_bytes, s>>>(
+        P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
+        reinterpret_cast<unsigned long long *>(d_counts), mode64);
     TC_CUDA(cudaGetLastError());
     *launches += 1;
     BinLists lists;
@@ -189,6 +235,9 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     lists.ntiles = ntiles;
     lists.w = wl.p;
     lists.w_count = stats.p;
+    lists.du = P.du;
+    lists.de = P.de;
+    lists.dpb = P.dpb;
     st = launch_bins(g, lists, s, d_counts, prof ? ev + 1 : nullptr, launches, mode64);
     if (st != TC_OK) return st;
     if (prof) {

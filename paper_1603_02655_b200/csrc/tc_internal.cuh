@@ -4,11 +4,14 @@
 //   off[n+1]   uint32 row offsets of the symmetric neighbour CSR
 //   adj[2D]    uint32 entries (w << 2) | tag, each row sorted by w;
 //              tag bit0 = u->w, bit1 = w->u (the 2-bit direction code)
-//   dyad_u[D], dyad_e[D], dyad_c[D]   canonical dyads (u < v) in canonical
-//              order (u ascending, v ascending): row u, the entry
-//              of v in row u, e = (v << 2) | pre with pre = IsEdge(u,v) +
-//              2 IsEdge(v,u) (v0.4), and the uniform cost
-//              c = |N(u)| + |N(v)|
+//   ups[n]     uint32 index in adj of the first entry w > u of row u
+//   dyad_u[D], dyad_e[D], dyad_c[D], dyad_pb[D], dyad_t[D]   canonical
+//              dyads (u < v) in canonical order (u ascending, v ascending,
+//              P:277-281): row u, the entry of v in row u, e = (v << 2) | pre
+//              with pre = IsEdge(u,v) + 2 IsEdge(v,u) (v0.4), the
+//              uniform cost c = |N(u)| + |N(v)|, the index in adj of
+//              the first entry w > u of row v, and the merge length
+//              t = |{w in N(u): w > u}| + |{w in N(v): w > u}| (census.cu)
 #pragma once
 
 #include <cuda_runtime.h>
@@ -78,11 +81,11 @@ constexpr int kNumBins = 2;
 // (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
 constexpr uint64_t kShardKappa = 8;
 
-struct BinItem2 {   // thread bin: dyad (u, e)
-    uint32_t u, e;
+struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, merge length t
+    uint32_t pa, pb, e, t;
 };
-struct BinItem4 {   // warp bin: dyad (u, e) and its merge diagonals [d0, d1)
-    uint32_t u, e, d0, d1;
+struct BinItemW {   // warp bin: dyad index (in the planned range), diagonals [d0, d1)
+    uint32_t k, d0, d1, pad;
 };
 
 }  // namespace tc
@@ -98,6 +101,9 @@ struct tc_graph {
     uint32_t *dyad_u = nullptr; size_t dyad_n = 0;
     uint32_t *dyad_e = nullptr;
     uint32_t *dyad_c = nullptr;
+    uint32_t *dyad_pb = nullptr;
+    uint32_t *dyad_t = nullptr;
+    uint32_t *ups = nullptr;   size_t ups_n = 0;
     int profile = 0;
     tc_profile prof{};
     uint64_t launches = 0;

@@ -101,20 +101,75 @@ def test_full_config_vs_golden(tcb, golden_dir, name):
     assert st == rec["stats"]
 
 
+def attributed_range(n, src, dst, b, e):
+    """Classes 012 / 102 of canonical dyads [b, e) as the CUDA path attributes
+    them (reading 14), restated from sets, for small graphs: dyad
+    (u, v) owns n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}|, plus one
+    dyadic triad of dyad (v, x) for every x > v in N(u) & N(v) (the
+    intersection element u < v of dyad (v, x), met by this merge).  The sum
+    over any partition of [0, D) is the paper's n - |S| - 2 total."""
+    arcs = {(int(s), int(d)) for s, d in zip(src, dst) if s != d}
+    nb = {}
+    for s, d in arcs:
+        nb.setdefault(s, set()).add(d)
+        nb.setdefault(d, set()).add(s)
+    mutual = lambda x, y: (x, y) in arcs and (y, x) in arcs
+    dyads = sorted({(min(s, d), max(s, d)) for s, d in arcs})
+    out = [0, 0]
+    for u, v in dyads[b:e]:
+        common = nb[u] & nb[v]
+        own = n - len(nb[u]) - len(nb[v]) + sum(1 for x in common if x > u)
+        out[1 if mutual(u, v) else 0] += own
+        for x in common:
+            if x > v:
+                out[1 if mutual(v, x) else 0] += 1
+    return out
+
+
+def test_dyad_range_attribution_small(tcb):
+    # every class of a dyad range, exact, on small random digraphs
+    for seed in range(6):
+        a = synth.random_digraph(60 + 20 * seed, 0.08 + 0.02 * seed, seed=100 + seed)
+        og = oracle.Graph(a.n, a.src, a.dst)
+        D = og.stats()["dyads"]
+        g = tcb.tc_graph_create(a.n, a.src, a.dst)
+        rng = np.random.default_rng(seed)
+        bounds = sorted({0, D, *[int(x) for x in rng.integers(0, D, size=5)]})
+        tot = [0] * 16
+        for b, e in zip(bounds[:-1], bounds[1:]):
+            part = tcb.tc_census_range(g, b, e)
+            want = og.census_range(b, e)
+            assert part[3:] == want[3:], (seed, b, e)
+            assert part[1:3] == attributed_range(a.n, a.src, a.dst, b, e), (seed, b, e)
+            assert part[0] == 0
+            tot = [x + y for x, y in zip(tot, part)]
+        assert tcb.tc_close_census(a.n, tot) == og.census()
+        g.close()
+
+
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_dyad_range_parity(tcb, name):
-    # T6: random canonical-dyad ranges, GPU partial == oracle partial
+    # T6: random canonical-dyad ranges: classes 021D..300 equal the oracle's
+    # partial exactly; 012 / 102 move between ranges (DESIGN.md reading 14),
+    # so they are checked through a partition of [0, D) that sums to the census
     a = synth.make_config(name)
     og = oracle.Graph(a.n, a.src, a.dst)
     D = og.stats()["dyads"]
     g = tcb.tc_graph_create(a.n, a.src, a.dst)
     rng = np.random.default_rng(1)
+    cuts = [0]
     for _ in range(4):
-        b = int(rng.integers(0, D))
+        b = int(rng.integers(cuts[-1], D))
         e = min(D, b + int(rng.integers(1, 20_000)))
-        assert tcb.tc_census_range(g, b, e) == og.census_range(b, e), (b, e)
-    assert tcb.tc_census_range(g, D - 3, D + 100) == og.census_range(D - 3, D)
+        assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:], (b, e)
+        cuts += [b, e]
+    assert tcb.tc_census_range(g, D - 3, D + 100)[3:] == og.census_range(D - 3, D)[3:]
     assert tcb.tc_census_range(g, 5, 5) == [0] * 16
+    cuts = sorted(set(cuts + [D]))
+    tot = [0] * 16
+    for b, e in zip(cuts[:-1], cuts[1:]):
+        tot = [x + y for x, y in zip(tot, tcb.tc_census_range(g, b, e))]
+    assert tcb.tc_close_census(a.n, tot) == og.census()
     g.close()
 
 
