@@ -358,6 +358,10 @@ def run_ours(args):
             "phases_ms": {"build": build_ms, "plan": plan_ms, "census_kernels": census_ms,
                           "bin_kernels": [float(x) for x in avg_k],
                           "census_arcs_per_s": m_arcs / ((plan_ms + census_ms) * 1e-3)},
+            "work": {"bin_dyads": [int(x) for x in bin_dyads],
+                     "bin_sum_c": [int(x) for x in bin_work],
+                     "bin_merge_trips": [int(profs[-1]["bin_work"][2]),
+                                         int(profs[-1]["bin_work"][3])]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": names[dom],
                          "bytes_alg_per_launch": bytes_alg,

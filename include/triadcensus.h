@@ -96,7 +96,10 @@ typedef struct {
     float census_ms;        /* a3+a4: all bin kernels incl. histogram flush */
     float kernel_ms[4];     /* a3+a4 per bin: [0] thread bin, [1] warp bin, [2..3] 0 */
     uint64_t bin_items[4];  /* [0] thread-bin dyads, [1] warp items, [2] warp-bin dyads */
-    uint64_t bin_work[4];   /* sum of |N(u)|+|N(v)|: [0] thread bin, [1] warp bin */
+    uint64_t bin_work[4];   /* [0] / [1] thread / warp bin: sum of |N(u)|+|N(v)| (the
+                               paper's uniform work unit, SURVEY 8(d) B_alg);
+                               [2] / [3]: merge trips actually walked (entries
+                               w > u of both rows, census.cu) */
 } tc_profile;
 
 /* Build the device graph from an arc list (a1).

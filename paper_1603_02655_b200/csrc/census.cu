@@ -78,8 +78,9 @@ __device__ __forceinline__ void add_dyadic(Acc &c, uint32_t pre, uint64_t x) {
     else c.dy012 += x;
 }
 
+// nibbles -> bytes (nibble 0 is moved to the dyadic counters by the caller)
 __device__ __forceinline__ void spill(Acc &c) {
-    c.ev8 += c.n4 & kNib;
+    c.ev8 += c.n4 & (kNib & ~0xFull);
     c.od8 += (c.n4 >> 4) & kNib;
     c.n4 = 0;
 }
@@ -128,7 +129,7 @@ __device__ __forceinline__ uint32_t merge_path(const uint32_t *__restrict__ A, u
 // Classify merge diagonals [d0, d1) of dyad (u, v).  A = adj[oa, oa+a) (the
 // entries w > u of N(u)), B = adj[ob, ob+b) (the entries w > u of N(v)),
 // both followed by more of their row and a sentinel; kv = v<<2|3; tab =
-// shared address of the 64-entry uint64 increment table.  The caller has
+// shared address of the 128-entry uint64 increment table.  The caller has
 // reserved d1 - d0 byte-counter increments (warp_reserve).
 __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uint32_t oa,
                                            uint32_t a, uint32_t ob, uint32_t b, uint32_t kv,
@@ -141,7 +142,7 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     // current heads and the next elements (sentinel-terminated rows)
     uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
     uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
-    uint32_t I = 0;
+    // table row of this pre: 128 entries (canonical << 6 | code), 8 bytes each
     const uint32_t tabp = tab + 8u * pre;
     uint32_t t = d0;
     while (t < d1) {
@@ -156,8 +157,7 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
             // A element: w > v.  B-only element: canonical unless it is the
             // B twin of the A element just consumed (classified already).
             const bool canon = ta ? (kx > kv) : (ky != lastA);
-            I += (uint32_t)(ta & tb);
-            c.n4 += canon ? lds_u64(tabp + (ca | cb)) : 0ull;
+            c.n4 += lds_u64(tabp + (ca | cb | (canon ? 512u : 0u)));
             lastA = ta ? kx : lastA;
             pa += ta;
             pb += !ta;
@@ -167,21 +167,31 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
             y = ta ? y : yn;
             yn = ta ? yn : nv;
         }
+        // nibble 0 counts this dyad's intersection elements w > u (own-I)
+        add_dyadic(c, pre, c.n4 & 15u);
         spill(c);
     }
-    add_dyadic(c, pre, I);
 }
 
-// shared increment table: code -> one nibble at 4 * class, plus (both tags
-// set: a canonical intersection element w > v) one nibble at class 102 if
-// tv == 3 else 012, the dyadic triad owed to dyad (v, w); per-warp totals
+// shared increment table, 128 entries (canonical << 6 | code):
+//   non-canonical, both tags set (an intersection element u < w < v):
+//     nibble 0 (the dyad's own intersection count I, moved to 012 / 102 by
+//     pre at every spill);
+//   canonical: one nibble at 4 * class, and, both tags set (an intersection
+//     element w > v), nibble 0 plus one nibble at class 102 if tv == 3 else
+//     012 (the dyadic triad owed to dyad (v, w)).
+// Every nibble gets at most 1 per trip.  wsh: per-warp totals.
 __device__ __forceinline__ void block_setup(unsigned long long *tab,
                                             unsigned long long (*wsh)[16]) {
-    if (threadIdx.x < 64) {
-        const uint32_t code = threadIdx.x, tu = (code >> 2) & 3u, tv = code >> 4;
-        unsigned long long inc = 1ull << (4u * c_triad_table[code]);
-        if (tu && tv) inc += 1ull << (tv == 3u ? 8u : 4u);
-        tab[code] = inc;
+    if (threadIdx.x < 128) {
+        const uint32_t code = threadIdx.x & 63u, canon = threadIdx.x >> 6;
+        const uint32_t tu = (code >> 2) & 3u, tv = code >> 4;
+        unsigned long long inc = (tu && tv) ? 1ull : 0ull;
+        if (canon) {
+            inc += 1ull << (4u * c_triad_table[code]);
+            if (tu && tv) inc += 1ull << (tv == 3u ? 8u : 4u);
+        }
+        tab[threadIdx.x] = inc;
     }
     for (int i = threadIdx.x; i < kWarps * 16; i += blockDim.x) (&wsh[0][0])[i] = 0;
     __syncthreads();
@@ -242,7 +252,7 @@ __device__ __forceinline__ WarpDyad warp_dyad(const BinLists &L, const uint32_t 
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
                 uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
-    __shared__ unsigned long long tab_s[64];
+    __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
@@ -274,7 +284,7 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
               const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
-    __shared__ unsigned long long tab_s[64];
+    __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);

@@ -34,10 +34,23 @@ rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask
     for (int i = threadIdx.x; i < radix; i += kRsThreads) h[i] = 0;
     __syncthreads();
     const size_t base = (size_t)blockIdx.x * kRsTile;
+    if (base + kRsTile <= n) {
+        // full tile: all 16 keys in flight as 8 x 16-byte loads, then count
+        const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(keys + base);
+        ulonglong2 v[kRsItems / 2];
+#pragma unroll
+        for (int k = 0; k < kRsItems / 2; k++) v[k] = __ldcs(k2 + k * kRsThreads + threadIdx.x);
+#pragma unroll
+        for (int k = 0; k < kRsItems / 2; k++) {
+            atomicAdd(&h[(uint32_t)(v[k].x >> shift) & mask], 1u);
+            atomicAdd(&h[(uint32_t)(v[k].y >> shift) & mask], 1u);
+        }
+    } else {
 #pragma unroll 4
-    for (int k = 0; k < kRsItems; k++) {
-        size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
-        if (i < n) atomicAdd(&h[(uint32_t)(__ldg(keys + i) >> shift) & mask], 1u);
+        for (int k = 0; k < kRsItems; k++) {
+            size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
+            if (i < n) atomicAdd(&h[(uint32_t)(__ldg(keys + i) >> shift) & mask], 1u);
+        }
     }
     __syncthreads();
     for (int d = threadIdx.x; d < radix; d += kRsThreads) hist[(size_t)d * ntiles + blockIdx.x] = h[d];

@@ -41,7 +41,9 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t c) {
 // also adds every dyad's dyadic term n - |N(u)| - |N(v)| (the
 // census kernels add the intersection part) to d_counts, by class
 // (mode16: 012 / 102) or by code pre (mode64).
-// stats: [0] warp items, [1] thread-bin work, [2] warp-bin work, [3] big dyads
+// stats: [0] warp items, [1] / [2] thread- / warp-bin sum of c = |N(u)|+|N(v)|
+// (the algorithmic work unit), [3] big dyads, [4] / [5] thread- / warp-bin
+// merge trips (sum of t)
 struct PlanIn {
     const uint32_t *du, *de, *dc, *dt, *dpb, *ups, *off;
 };
@@ -98,7 +100,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     }
     __syncthreads();
     extern __shared__ uint4 stage[];   // the tile's thread list, staged for coalesced stores
-    unsigned long long wt = 0, ww = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
+    unsigned long long wt = 0, ww = 0, tt = 0, tw = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
 #pragma unroll 4
     for (int k = 0; k < kPlanItems; k++) {
         const uint64_t i = tile0 + wbase + k * 32 + lane;
@@ -107,16 +109,19 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         uint32_t nch = 0;
         if (valid) {
             const uint32_t u = __ldg(P.du + i), e = __ldg(P.de + i), pre = e & 3u;
-            const unsigned long long dy = n - __ldg(P.dc + i);
+            const uint32_t cf = __ldg(P.dc + i);
+            const unsigned long long dy = n - cf;
             dy1 += pre == 1u ? dy : 0ull;
             dy2 += pre == 2u ? dy : 0ull;
             dy3 += pre == 3u ? dy : 0ull;
             if (d < 255u) {
                 stage[wc[warp][d] + rank[k]] = make_uint4(__ldg(P.ups + u), __ldg(P.dpb + i), e, c);
-                wt += c;
+                wt += cf;
+                tt += c;
             } else {
                 nch = (c + kWarpChunk - 1) / kWarpChunk;
-                ww += c;
+                ww += cf;
+                tw += c;
                 nbig++;
             }
         }
@@ -146,6 +151,8 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         wt += __shfl_xor_sync(0xffffffffu, wt, o);
         ww += __shfl_xor_sync(0xffffffffu, ww, o);
         nbig += __shfl_xor_sync(0xffffffffu, nbig, o);
+        tt += __shfl_xor_sync(0xffffffffu, tt, o);
+        tw += __shfl_xor_sync(0xffffffffu, tw, o);
         dy1 += __shfl_xor_sync(0xffffffffu, dy1, o);
         dy2 += __shfl_xor_sync(0xffffffffu, dy2, o);
         dy3 += __shfl_xor_sync(0xffffffffu, dy3, o);
@@ -154,6 +161,8 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         if (wt) atomicAdd(&stats[1], wt);
         if (ww) atomicAdd(&stats[2], ww);
         if (nbig) atomicAdd(&stats[3], nbig);
+        if (tt) atomicAdd(&stats[4], tt);
+        if (tw) atomicAdd(&stats[5], tw);
         if (mode64) {
             if (dy1) atomicAdd(&d_counts[1], dy1);
             if (dy2) atomicAdd(&d_counts[2], dy2);
@@ -217,8 +226,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
-    if ((st = stats.allocate(mem, 4)) != TC_OK) return st;
-    TC_CUDA(cudaMemsetAsync(stats.p, 0, 4 * sizeof(unsigned long long), s));
+    if ((st = stats.allocate(mem, 6)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(stats.p, 0, 6 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off};
     const int stage_bytes = kPlanTile * (int)sizeof(BinItemT);
@@ -242,7 +251,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if (st != TC_OK) return st;
     if (prof) {
         TC_CUDA(cudaEventRecord(ev[3], s));
-        unsigned long long hs[4];
+        unsigned long long hs[6];
         TC_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
         const uint64_t nt = N - hs[3];
@@ -262,7 +271,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->bin_items[3] = 0;
         prof->bin_work[0] = hs[1];
         prof->bin_work[1] = hs[2];
-        prof->bin_work[2] = prof->bin_work[3] = 0;
+        prof->bin_work[2] = hs[4];
+        prof->bin_work[3] = hs[5];
         for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
     }
     return TC_OK;
