@@ -155,7 +155,7 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
  * n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}| to its class, plus one
  * to the class of dyad (v,x) for every x > v in N(u) & N(v) -- the
  * intersection element u of that later dyad, which its own merge (starting
- * at entries > v) does not see (reading 14).  Synchronous. */
+ * at entries > v) does not see (reading 21).  Synchronous. */
 tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                           void *cuda_stream, uint64_t partial[16]);
 

@@ -22,7 +22,7 @@
 //     intersection element v > u -- so every canonical intersection element
 //     w > v of dyad (u, v) also adds the dyadic triad (v, w, u-excluded)
 //     owed to dyad (v, w): one to class 102 if tv == 3 (v <-> w mutual),
-//     else to class 012 (reading 14).  Each triangle's three
+//     else to class 012 (reading 21).  Each triangle's three
 //     intersections are thus counted exactly once, and the census is the
 //     paper's; only the split of 012/102 between dyad ranges moves.
 //

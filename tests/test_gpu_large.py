@@ -47,5 +47,5 @@ def test_c4_sampled_ranges_vs_oracle(c4):
     ranges = [(max(0, hub - 3), hub + 3)]
     ranges += [(int(b), int(b) + 2000) for b in rng.integers(0, D - 2000, size=3)]
     for b, e in ranges:
-        # classes 021D..300 per range exactly (012/102 move, reading 14)
+        # classes 021D..300 per range exactly (012/102 move, reading 21)
         assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:], (b, e)

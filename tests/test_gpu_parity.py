@@ -103,7 +103,7 @@ def test_full_config_vs_golden(tcb, golden_dir, name):
 
 def attributed_range(n, src, dst, b, e):
     """Classes 012 / 102 of canonical dyads [b, e) as the CUDA path attributes
-    them (reading 14), restated from sets, for small graphs: dyad
+    them (reading 21), restated from sets, for small graphs: dyad
     (u, v) owns n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}|, plus one
     dyadic triad of dyad (v, x) for every x > v in N(u) & N(v) (the
     intersection element u < v of dyad (v, x), met by this merge).  The sum
@@ -150,7 +150,7 @@ def test_dyad_range_attribution_small(tcb):
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_dyad_range_parity(tcb, name):
     # T6: random canonical-dyad ranges: classes 021D..300 equal the oracle's
-    # partial exactly; 012 / 102 move between ranges (reading 14),
+    # partial exactly; 012 / 102 move between ranges (reading 21),
     # so they are checked through a partition of [0, D) that sums to the census
     a = synth.make_config(name)
     og = oracle.Graph(a.n, a.src, a.dst)

@@ -1,6 +1,6 @@
 """Summarise gpurun_out/ ncu artefacts into profiles/ (tracked).
 
-    python tools/make_profiles.py <round-tag> <launches.csv> <full.ncu-rep> [config]
+    python tools/make_profiles.py <round-tag> <launches.csv> <full.ncu-rep[,more.ncu-rep]> [config]
 """
 import json, os, subprocess, sys
 sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
@@ -18,7 +18,7 @@ with open(os.path.join(out, "%s_launches_%s.txt" % (tag, cfg)), "w") as f:
             "# per-launch times are cold-cache and serialised: compare SHARES, not absolutes\n"
             "# total_us  share  launches  us_per_launch  kernel\n" % cfg)
     f.write(txt)
-summ = summary(rep)
+summ = [d for r in rep.split(",") for d in summary(r)]
 with open(os.path.join(out, "%s_ncu_full_%s.json" % (tag, cfg)), "w") as f:
     json.dump(summ, f, indent=1)
 traffic = {}
