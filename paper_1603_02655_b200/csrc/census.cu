@@ -220,7 +220,8 @@ __device__ __forceinline__ void block_finish(Acc &c, unsigned long long (*wsh)[1
     }
 }
 
-// prefetch the 128-byte lines of adj[o, o+len] into L2 (fire and forget)
+// prefetch the 128-byte lines of adj[o, o+len] into L2 (fire and forget;
+// prefetch.global.L1 measured no different)
 __device__ __forceinline__ void prefetch_row_l2(const uint32_t *adj, uint32_t o, uint32_t len) {
     const char *p = reinterpret_cast<const char *>(adj + o);
     const char *e = reinterpret_cast<const char *>(adj + o + len);
@@ -245,13 +246,29 @@ __device__ __forceinline__ WarpDyad warp_dyad(const BinLists &L, const uint32_t 
     return w;
 }
 
+// Thread-bin work is handed out dynamically: a block takes the next unit
+// (a quarter of a plan tile, kUnitDyads slots of one tile, in canonical tile
+// order) from a global cursor, so the kernel's tail is at most one unit per
+// resident block instead of a static round-robin's extra tiles.
+constexpr uint32_t kUnitsPerTile = 4;
+constexpr uint32_t kUnitDyads = kPlanTile / kUnitsPerTile;
+static_assert(kUnitDyads % kCensusThreads == 0, "unit = whole block rounds");
+
+__device__ __forceinline__ uint64_t next_unit(unsigned long long *cursor, uint32_t *unit_s) {
+    __syncthreads();   // every warp is done with the previous unit's unit_s
+    if (threadIdx.x == 0) *unit_s = (uint32_t)atomicAdd(cursor, 1ull);
+    __syncthreads();
+    return *unit_s;
+}
+
 // thread bin: one thread per dyad.  Block-persistent over tiles of
 // kPlanTile consecutive canonical dyads; inside a tile the plan ordered the
 // thread-bin dyads by merge length, so each warp's lanes run equal trip
 // counts while the tile keeps the N(u) rows of nearby u hot in L1/L2.
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
-                uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
+                uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts,
+                unsigned long long *cursor) {
     __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup(tab_s, wsh);
@@ -259,10 +276,14 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
     Acc c;
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t cnt = __ldg(tile_count + tile);
+    __shared__ uint32_t unit_s;
+    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * kUnitsPerTile;
+         unit = next_unit(cursor, &unit_s)) {
+        const uint64_t tile = unit / kUnitsPerTile;
+        const uint32_t part = (uint32_t)(unit % kUnitsPerTile) * kUnitDyads;
+        const uint32_t cnt = min(__ldg(tile_count + tile), part + kUnitDyads);
         const BinItemT *it = items + tile * kPlanTile;
-        for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
+        for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
             BinItemT e{0, 0, 0, 0};
             if (valid) {
@@ -279,6 +300,14 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
     block_finish(c, wsh, d_counts);
 }
 
+// warp bin: a warp takes the next item from a global cursor (dynamic, so
+// the tail is one item per resident warp)
+__device__ __forceinline__ uint64_t next_item(unsigned long long *cursor) {
+    unsigned long long it = 0;
+    if ((threadIdx.x & 31) == 0) it = atomicAdd(cursor, 1ull);
+    return __shfl_sync(0xffffffffu, it, 0);
+}
+
 // warp bin: one warp per item = one dyad's diagonals [d0, d1), 32 lane
 // segments of <= kLaneSpan diagonals each
 __global__ void __launch_bounds__(kCensusThreads)
@@ -292,9 +321,7 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t count = *L.w_count;
-    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t it = wid; it < count; it += nw) {
+    for (uint64_t it = next_item(L.wcursor); it < count; it = next_item(L.wcursor)) {
         const BinItemW e = L.w[it];
         const WarpDyad w = warp_dyad(L, off, ups, e.k);
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
@@ -404,15 +431,20 @@ __device__ __forceinline__ void block_finish64(Smem64 &S, Acc64 &c, unsigned lon
 
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_thread64(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
-                  uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
+                  uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts,
+                  unsigned long long *cursor) {
     __shared__ Smem64 S;
     block_setup64(S);
     Acc64 c{{0, 0, 0}, 0};
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const uint32_t cnt = __ldg(tile_count + tile);
+    __shared__ uint32_t unit_s;
+    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * kUnitsPerTile;
+         unit = next_unit(cursor, &unit_s)) {
+        const uint64_t tile = unit / kUnitsPerTile;
+        const uint32_t part = (uint32_t)(unit % kUnitsPerTile) * kUnitDyads;
+        const uint32_t cnt = min(__ldg(tile_count + tile), part + kUnitDyads);
         const BinItemT *it = items + tile * kPlanTile;
-        for (uint32_t base = warp * 32; base < cnt; base += kCensusThreads) {
+        for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
             BinItemT e{0, 0, 0, 0};
             if (valid) e = it[base + lane];
@@ -433,9 +465,7 @@ k_census_warp64(const BinLists L, const uint32_t *__restrict__ off,
     Acc64 c{{0, 0, 0}, 0};
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint64_t count = *L.w_count;
-    const uint64_t wid = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t it = wid; it < count; it += nw) {
+    for (uint64_t it = next_item(L.wcursor); it < count; it = next_item(L.wcursor)) {
         const BinItemW e = L.w[it];
         const WarpDyad w = warp_dyad(L, off, ups, e.k);
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
@@ -452,15 +482,33 @@ k_census_warp64(const BinLists L, const uint32_t *__restrict__ off,
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
                       cudaEvent_t *ev, uint64_t *launches, int mode64) {
     unsigned long long *out = reinterpret_cast<unsigned long long *>(d_counts);
-    int sms = 148;
+    int sms = 148, per = 0, perw = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
-    const unsigned grid = (unsigned)sms * kCensusBlocksPerSM;
+    // warp bin: one resident wave, items handed out by bl.wcursor
+    if (mode64)
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perw, k_census_warp64,
+                                                              kCensusThreads, 0));
+    else
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perw, k_census_warp,
+                                                              kCensusThreads, 0));
+    const unsigned grid = (unsigned)sms * (unsigned)(perw > 0 ? perw : 1);
+    // thread bin: one resident wave, units handed out by bl.cursor
+    if (mode64)
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_census_thread64,
+                                                              kCensusThreads, 0));
+    else
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_census_thread,
+                                                              kCensusThreads, 0));
+    const uint64_t units = bl.ntiles * kUnitsPerTile;
+    uint64_t tgrid = (uint64_t)sms * (per > 0 ? per : 1);
+    if (tgrid > units) tgrid = units ? units : 1;
     if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
     if (mode64)
-        k_census_thread64<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->adj,
-                                                         out);
+        k_census_thread64<<<(unsigned)tgrid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles,
+                                                                    g->adj, out, bl.cursor);
     else
-        k_census_thread<<<grid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles, g->adj, out);
+        k_census_thread<<<(unsigned)tgrid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles,
+                                                                  g->adj, out, bl.cursor);
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
     if (mode64)

@@ -12,6 +12,8 @@ struct BinLists {
     uint64_t ntiles = 0;                    // tiles of kPlanTile canonical dyads
     const BinItemW *w = nullptr;            // warp bin: <= kWarpChunk diagonals per item
     const unsigned long long *w_count = nullptr;   // device: number of warp-bin items
+    unsigned long long *cursor = nullptr;   // device, zeroed: thread-bin unit dispatch cursor
+    unsigned long long *wcursor = nullptr;  // device, zeroed: warp-bin item dispatch cursor
     const uint32_t *du = nullptr, *de = nullptr, *dpb = nullptr;   // dyad arrays of the range
 };
 
@@ -19,7 +21,6 @@ constexpr int kCensusThreads = 256;
 constexpr int kPlanThreads = 256;
 constexpr int kPlanItems = 16;
 constexpr int kPlanTile = kPlanThreads * kPlanItems;   // canonical dyads per plan tile
-constexpr unsigned kCensusBlocksPerSM = 8;
 
 
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]

@@ -226,8 +226,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
-    if ((st = stats.allocate(mem, 6)) != TC_OK) return st;
-    TC_CUDA(cudaMemsetAsync(stats.p, 0, 6 * sizeof(unsigned long long), s));
+    if ((st = stats.allocate(mem, 8)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(stats.p, 0, 8 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off};
     const int stage_bytes = kPlanTile * (int)sizeof(BinItemT);
@@ -244,6 +244,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     lists.ntiles = ntiles;
     lists.w = wl.p;
     lists.w_count = stats.p;
+    lists.cursor = stats.p + 6;
+    lists.wcursor = stats.p + 7;
     lists.du = P.du;
     lists.de = P.de;
     lists.dpb = P.dpb;
