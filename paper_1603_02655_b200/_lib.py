@@ -11,6 +11,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtriadcensus.so")
+# dev only (tools/ab.sh): same-box A/B timing of a variant build of the library
+if os.environ.get("TC_LIB_VARIANT"):
+    LIB_PATH = os.path.abspath(os.environ["TC_LIB_VARIANT"])
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -91,6 +91,17 @@ __device__ __forceinline__ uint64_t lds_u64(uint32_t addr) {
     return v;
 }
 
+// v = canonical ? shared u64 at addr : dflt (the load is predicated off, so
+// non-canonical lanes cost no shared-memory wavefront)
+__device__ __forceinline__ uint64_t lds_u64_if(uint32_t addr, bool p, uint64_t dflt) {
+    uint64_t v = dflt;
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.shared.u64 %0, [%1];\n\t}"
+        : "+l"(v)
+        : "r"(addr), "r"((uint32_t)p));
+    return v;
+}
+
 // Warp-level flush (all 32 lanes active): each class 1..15 is summed over
 // the warp with one REDUX and lane 0 adds it to the warp's own shared slots
 // (plain adds; 64-bit shared atomics are CAS loops on sm_100).
@@ -131,6 +142,7 @@ __device__ __forceinline__ uint32_t merge_path(const uint32_t *__restrict__ A, u
 // both followed by more of their row and a sentinel; kv = v<<2|3; tab =
 // shared address of the 128-entry uint64 increment table.  The caller has
 // reserved d1 - d0 byte-counter increments (warp_reserve).
+template <bool PRED>
 __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uint32_t oa,
                                            uint32_t a, uint32_t ob, uint32_t b, uint32_t kv,
                                            uint32_t pre, uint32_t d0, uint32_t d1, uint32_t tab,
@@ -142,8 +154,9 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     // current heads and the next elements (sentinel-terminated rows)
     uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
     uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
-    // table row of this pre: 128 entries (canonical << 6 | code), 8 bytes each
-    const uint32_t tabp = tab + 8u * pre;
+    // canonical increments of this pre: 16 entries (tu | tv << 2), 8 bytes each,
+    // one 128-byte bank row
+    const uint32_t tabp = PRED ? tab + 128u * pre : tab + 8u * pre;
     uint32_t t = d0;
     while (t < d1) {
         const uint32_t lim = min(d1, t + 15u);   // nibble counters hold 15
@@ -151,13 +164,19 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
             const uint32_t kx = x | 3u, ky = y | 3u;
             const bool ta = kx <= ky;            // consume A (ties: A first)
             const bool tb = ky <= kx;            // B's id is the merged id
-            // 8 * (code - pre) = tu<<5 | tv<<7, tu = tag in A, tv = tag in B
-            const uint32_t ca = ta ? ((x << 5) & 0x60u) : 0u;
-            const uint32_t cb = tb ? ((y << 7) & 0x180u) : 0u;
+            // tu = tag in A, tv = tag in B; PRED: 8 * (tu | tv << 2), else
+            // 8 * (code - pre) = tu << 5 | tv << 7
+            const uint32_t ca = ta ? ((x << (PRED ? 3 : 5)) & (PRED ? 0x18u : 0x60u)) : 0u;
+            const uint32_t cb = tb ? ((y << (PRED ? 5 : 7)) & (PRED ? 0x60u : 0x180u)) : 0u;
             // A element: w > v.  B-only element: canonical unless it is the
             // B twin of the A element just consumed (classified already).
             const bool canon = ta ? (kx > kv) : (ky != lastA);
-            c.n4 += lds_u64(tabp + (ca | cb | (canon ? 512u : 0u)));
+            // non-canonical: an intersection element u < w < v adds nibble 0
+            // (own I); only canonical trips read the table (predicated LDS)
+            if (PRED)
+                c.n4 += lds_u64_if(tabp + (ca | cb), canon, (ta && tb) ? 1ull : 0ull);
+            else   // thread bin: unpredicated, non-canonical half of the table
+                c.n4 += lds_u64(tabp + (ca | cb | (canon ? 512u : 0u)));
             lastA = ta ? kx : lastA;
             pa += ta;
             pb += !ta;
@@ -173,25 +192,29 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     }
 }
 
-// shared increment table, 128 entries (canonical << 6 | code):
-//   non-canonical, both tags set (an intersection element u < w < v):
-//     nibble 0 (the dyad's own intersection count I, moved to 012 / 102 by
-//     pre at every spill);
-//   canonical: one nibble at 4 * class, and, both tags set (an intersection
-//     element w > v), nibble 0 plus one nibble at class 102 if tv == 3 else
-//     012 (the dyadic triad owed to dyad (v, w)).
-// Every nibble gets at most 1 per trip.  wsh: per-warp totals.
+// shared increment tables: thread bin: 128 entries (canonical << 6 | code);
+// warp bin: 64 entries (pre << 4 | tu | tv << 2), canonical trips only; code = pre | tu << 2 | tv << 4: one nibble at 4 * class, and,
+// both tags set (an intersection element w > v), nibble 0 (own I) plus one
+// nibble at class 102 if tv == 3 else 012 (the dyadic triad owed to dyad
+// (v, w)).  A non-canonical trip adds nibble 0 iff both tags are set (an
+// intersection element u < w < v; the dyad's own intersection count I,
+// moved to 012 / 102 by pre at every spill).  Every nibble gets at most 1
+// per trip.  The warp bin (one pre per warp) reads only the canonical half,
+// with a predicated load (a 128-byte bank row per pre: no bank conflicts);
+// the thread bin (mixed pre) measured faster with one unpredicated load.  wsh: per-warp totals.
+template <bool WARPBIN>
 __device__ __forceinline__ void block_setup(unsigned long long *tab,
                                             unsigned long long (*wsh)[16]) {
-    if (threadIdx.x < 128) {
+    if (threadIdx.x < (WARPBIN ? 64 : 128)) {
         const uint32_t code = threadIdx.x & 63u, canon = threadIdx.x >> 6;
         const uint32_t tu = (code >> 2) & 3u, tv = code >> 4;
         unsigned long long inc = (tu && tv) ? 1ull : 0ull;
-        if (canon) {
+        if (canon || WARPBIN) {
             inc += 1ull << (4u * c_triad_table[code]);
             if (tu && tv) inc += 1ull << (tv == 3u ? 8u : 4u);
         }
-        tab[threadIdx.x] = inc;
+        if (WARPBIN) tab[(code & 3u) << 4 | tu | tv << 2] = inc;   // pre << 4 | tu | tv << 2
+        else tab[threadIdx.x] = inc;                               // canonical << 6 | code
     }
     for (int i = threadIdx.x; i < kWarps * 16; i += blockDim.x) (&wsh[0][0])[i] = 0;
     __syncthreads();
@@ -271,7 +294,7 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
                 unsigned long long *cursor) {
     __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
-    block_setup(tab_s, wsh);
+    block_setup<false>(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
@@ -294,7 +317,7 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
                 prefetch_row_l2(adj, e.pb, e.t);
             }
             warp_reserve(c, wsh[warp], e.t);
-            if (valid) merge_diag(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
+            if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
         }
     }
     block_finish(c, wsh, d_counts);
@@ -313,9 +336,9 @@ __device__ __forceinline__ uint64_t next_item(unsigned long long *cursor) {
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
               const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
-    __shared__ unsigned long long tab_s[128];
+    __shared__ unsigned long long tab_s[64];
     __shared__ unsigned long long wsh[kWarps][16];
-    block_setup(tab_s, wsh);
+    block_setup<true>(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
@@ -327,7 +350,7 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
         const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
         warp_reserve(c, wsh[warp], d1 - d0);
-        if (d0 < d1) merge_diag(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
+        if (d0 < d1) merge_diag<true>(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
     }
     block_finish(c, wsh, d_counts);
 }
