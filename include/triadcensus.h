@@ -184,6 +184,28 @@ tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint
  * world+1 entries). */
 tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds);
 
+/* The multithreaded version's task queues, as a GPU scheduler (SURVEY.md
+ * section 8(f) f3).  Fig. "Distributed Task Queue generation algorithm ...
+ * Canonical Dyad(uniform distr.)": NsetSize += |N[u]| + |N[v]|
+ * - 2; Fig. "... Canonical Dyad(non-uniform distr.)": NsetSize
+ * += |S|, S = N[u] U N[v] \ {u,v}.  Walking the canonical dyads in the
+ * algorithm's order, a queue is closed (thid + 1, NsetSize <- 0)
+ * right after the dyad that makes NsetSize > max_nset_size; queues are
+ * therefore contiguous dyad ranges, usable with tc_census_range.
+ *   starts      host array: starts[q] = first canonical dyad of the q-th
+ *               non-empty queue (a cut after the last dyad opens no queue);
+ *               queue q = [starts[q], starts[q+1]) with starts[nqueues] = D
+ *               implied.  Capacity `cap` entries (may be 0 with starts NULL
+ *               to query the count).
+ *   *nqueues    number of non-empty queues (always set on TC_OK/TC_E_RANGE)
+ *   *total_nset aggregate NsetSize over all dyads (Table)
+ * Errors: TC_E_INVALID (bad strategy / NULL outputs), TC_E_RANGE (more than
+ * cap queues; nothing written to starts).  Synchronous on the stream. */
+enum { TC_QUEUES_UNIFORM = 0, TC_QUEUES_NONUNIFORM = 1 };
+tc_status tc_task_queues(const tc_graph *g, int strategy, uint64_t max_nset_size,
+                         void *cuda_stream, uint64_t *starts, uint64_t cap, uint64_t *nqueues,
+                         uint64_t *total_nset);
+
 /* NCCL communicator.  Rank 0 calls tc_comm_unique_id, the 128 bytes are
  * broadcast by the caller (e.g. torch.distributed), then every rank calls
  * tc_comm_create.  NCCL is loaded lazily (libnccl.so.2, the copy torch

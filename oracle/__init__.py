@@ -71,6 +71,7 @@ def _load():
             lib.og_census64.argtypes = [vp, u64p, u64p]
             lib.og_bruteforce64.argtypes = [vp, u64p, u64p]
             lib.og_dyad_costs.argtypes = [vp, u64p]
+            lib.og_task_queues.argtypes = [vp, ctypes.c_int, u64, u64p, u64, u64p, u64p]
             lib.og_choose3_u128.argtypes = [u64, u64p, u64p]
             lib.og_graph_n.restype = u64
             lib.og_graph_m.restype = u64
@@ -176,6 +177,19 @@ class Graph:
         out = np.zeros(st["dyads"], np.uint64)
         self._lib.og_dyad_costs(self._h, _p(out, ctypes.c_uint64))
         return out
+
+    def task_queues(self, strategy: str, max_nset: int):
+        """The paper's task queues: (starts of the non-empty
+        queues in canonical dyad order, aggregate NsetSize)."""
+        strat = {"uniform": 0, "nonuniform": 1}[strategy]
+        cap = max(self.stats()["dyads"], 1)
+        starts = np.zeros(cap, np.uint64)
+        nq, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        rc = self._lib.og_task_queues(self._h, strat, int(max_nset), _p(starts, ctypes.c_uint64),
+                                      cap, ctypes.byref(nq), ctypes.byref(tot))
+        if rc != 0:
+            raise OracleError("og_task_queues failed (%d)" % rc)
+        return starts[:nq.value].copy(), int(tot.value)
 
     def neighbours_crs(self):
         nnz = int(self._lib.og_graph_nnz(self._h))

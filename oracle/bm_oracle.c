@@ -38,6 +38,14 @@
  *                    a,b are adjacent, else (a,c,b) (the canonical dyad that
  *                    counts it); a dyadic triple at its one connected
  *                    pair (x<y) with code pre(x,y); an empty triple at 0.
+ *   og_task_queues   the multithreaded version's task-queue generation
+ *                    (SURVEY.md 8(f) f3): Fig. "Distributed Task Queue
+ *                    generation ... Canonical Dyad(non-uniform distr.)"
+ *                    (NsetSize += |S|, S = N[u] U N[v] \ {u,v})
+ *                    and "... Canonical Dyad(uniform distr.)" (P:1676-1698:
+ *                    NsetSize += |N[u]| + |N[v]| - 2), line by line; a queue
+ *                    is closed (thid + 1, NsetSize <- 0) right after the dyad
+ *                    that makes NsetSize > MaxNsetSize.
  *
  * Graph sanitising (reading 9): self-loops are dropped,
  * duplicate arcs are merged.  Vertex ids are 0-based, n is explicit.
@@ -431,6 +439,72 @@ void og_dyad_costs(const og_graph *g, uint64_t *out)
             if (u < v)
                 out[k++] = (g->n_off[u + 1] - g->n_off[u]) + (g->n_off[v + 1] - g->n_off[v]);
         }
+}
+
+/* ------------------------------------------------------------------ */
+/* Task queues of the multithreaded version              */
+/* ------------------------------------------------------------------ */
+
+/* strategy 0 = Canonical Dyad(uniform distr.) (Fig. P:1676-1698),
+ * strategy 1 = Canonical Dyad(non-uniform distr.) (Fig. P:1650-1672).
+ * Queues are contiguous runs of canonical dyads (TQ[thid] <- TQ[thid] U
+ * <u,v> in the loop order of lines 4-6).  starts[q] = index of the first
+ * dyad of the q-th non-empty queue (q = 0 .. *nq - 1); a cut after the
+ * very last dyad opens no queue.  *total = aggregate NsetSize over all
+ * dyads (Table).  Returns 0, -1 (OOM), -2 (more than cap
+ * queues; *nq is still set). */
+int og_task_queues(const og_graph *g, int strategy, uint64_t max_nset, uint64_t *starts,
+                   uint64_t cap, uint64_t *nq, uint64_t *total)
+{
+    uint64_t n = g->n, maxd = 0;
+    for (uint64_t u = 0; u < n; u++) {
+        uint64_t d = g->n_off[u + 1] - g->n_off[u];
+        if (d > maxd) maxd = d;
+    }
+    uint32_t *S = (uint32_t *)malloc((2 * maxd + 1) * sizeof(uint32_t));
+    if (!S) return -1;
+    uint64_t thid = 0, nset = 0, k = 0, q = 0, tot = 0;
+    int open = 0;                                      /* TQ[thid] non-empty */
+    for (uint64_t u = 0; u < n; u++) {                 /* line 4 */
+        for (uint64_t a = g->n_off[u]; a < g->n_off[u + 1]; a++) {   /* line 5 */
+            uint64_t v = g->n_col[a];
+            if (!(u < v)) continue;                    /* line 6 */
+            if (!open) {                               /* line 7: TQ[thid] gets <u,v> */
+                if (q < cap) starts[q] = k;
+                q++;
+                open = 1;
+            }
+            uint64_t w;
+            if (strategy == 1) {                       /* lines 8-9: |S| */
+                uint64_t i = g->n_off[u], ie = g->n_off[u + 1];
+                uint64_t j = g->n_off[v], je = g->n_off[v + 1];
+                uint64_t s = 0;
+                while (i < ie || j < je) {
+                    uint64_t x;
+                    if (j >= je || (i < ie && g->n_col[i] < g->n_col[j])) x = g->n_col[i++];
+                    else if (i >= ie || g->n_col[j] < g->n_col[i]) x = g->n_col[j++];
+                    else { x = g->n_col[i]; i++; j++; }
+                    if (x != u && x != v) S[s++] = (uint32_t)x;
+                }
+                w = s;
+            } else {                                   /* line 8: |N[u]| + |N[v]| - 2 */
+                w = (g->n_off[u + 1] - g->n_off[u]) + (g->n_off[v + 1] - g->n_off[v]) - 2;
+            }
+            nset += w;
+            tot += w;
+            if (nset > max_nset) {                     /* lines 10-13 */
+                thid++;
+                nset = 0;
+                open = 0;
+            }
+            k++;
+        }
+    }
+    (void)thid;
+    free(S);
+    *nq = q;
+    *total = tot;
+    return q > cap ? -2 : 0;
 }
 
 /* ------------------------------------------------------------------ */

@@ -204,6 +204,20 @@ def tc_shard_bounds(g: Graph, world: int, stream=None) -> list[int]:
     return [int(x) for x in b]
 
 
+def tc_task_queues(g: Graph, strategy: str, max_nset_size: int, stream=None):
+    """The paper's task queues on the GPU: (starts of the
+    non-empty queues as a uint64 array in canonical dyad order, aggregate
+    NsetSize).  strategy: "uniform" or "nonuniform"."""
+    strat = {"uniform": 0, "nonuniform": 1}[strategy]
+    nq, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
+    cap = max(int(g.stats()["dyads"]), 1)     # never more queues than dyads
+    out = np.zeros(cap, np.uint64)
+    check(lib.tc_task_queues(g.handle, strat, int(max_nset_size), _stream_ptr(stream),
+                             out.ctypes.data_as(_lib.u64p), cap, ctypes.byref(nq),
+                             ctypes.byref(tot)), "tc_task_queues")
+    return out[:nq.value].copy(), int(tot.value)
+
+
 def tc_comm_unique_id() -> bytes:
     buf = (ctypes.c_uint8 * 128)()
     check(lib.tc_comm_unique_id(buf), "tc_comm_unique_id")

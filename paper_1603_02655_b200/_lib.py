@@ -63,6 +63,7 @@ _SIGS = {
     "tc_close_census": (cint, [u64, u64p, u64p]),
     "tc_shard_bounds_host": (cint, [u64p, u64, cint, u64, u64p]),
     "tc_shard_bounds": (cint, [vp, cint, vp, u64p]),
+    "tc_task_queues": (cint, [vp, cint, u64, vp, u64p, u64, u64p, u64p]),
     "tc_comm_unique_id": (cint, [ctypes.POINTER(ctypes.c_uint8)]),
     "tc_comm_create": (cint, [ctypes.POINTER(ctypes.c_uint8), cint, cint, cint, ctypes.POINTER(vp)]),
     "tc_comm_destroy": (None, [vp]),

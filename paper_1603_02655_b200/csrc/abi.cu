@@ -333,6 +333,20 @@ tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint
     return TC_OK;
 }
 
+tc_status tc_task_queues(const tc_graph *g, int strategy, uint64_t max_nset_size,
+                         void *cuda_stream, uint64_t *starts, uint64_t cap, uint64_t *nqueues,
+                         uint64_t *total_nset) {
+    if (!g || !nqueues || !total_nset || (strategy != TC_QUEUES_UNIFORM &&
+                                           strategy != TC_QUEUES_NONUNIFORM) ||
+        (cap && !starts)) {
+        set_error("invalid task-queue arguments");
+        return TC_E_INVALID;
+    }
+    TC_CUDA(cudaSetDevice(g->device));
+    return task_queues_device(g, strategy == TC_QUEUES_NONUNIFORM, max_nset_size,
+                              (cudaStream_t)cuda_stream, starts, cap, nqueues, total_nset);
+}
+
 tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds) {
     if (!g || !bounds || world < 1 || world > 1024) {
         set_error("invalid shard arguments");

@@ -18,6 +18,8 @@
 // The same costs, prefix-summed in canonical order, give the degree-balanced
 // multi-GPU shard cuts: the paper's uniform task
 // queues with one "queue" per GPU.
+#include <stdlib.h>
+
 #include "census.cuh"
 #include "scan.cuh"
 
@@ -194,6 +196,102 @@ __global__ void k_lower_bounds(const uint64_t *__restrict__ excl, uint64_t D,
     out[r] = lo;
 }
 
+
+// ---------------------------------------------------------------------------
+// the multithreaded version's task queues (Fig. P:1650-
+// 1672, Canonical Dyad(non-uniform distr.): NsetSize += |S|; Fig. P:1676-
+// 1698, Canonical Dyad(uniform distr.): NsetSize += |N[u]| + |N[v]| - 2) as
+// a GPU scheduler: queue q = a contiguous run of canonical dyads, closed
+// right after the dyad that makes its NsetSize exceed MaxNsetSize.
+// ---------------------------------------------------------------------------
+
+// per-dyad NsetSize: uniform |N(u)| + |N(v)| - 2 (dyad_c - 2); non-uniform
+// |S| = |N(u)| + |N(v)| - |N(u) & N(v)| - 2 (u and v are in the union).  One
+// warp per dyad: lanes take the entries of the shorter row and binary-search
+// them in the longer one (rows end in a sentinel; entries compare by id).
+__global__ void k_queue_weights(const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj,
+                                const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
+                                const uint32_t *__restrict__ dc, uint64_t D, int nonuniform,
+                                uint32_t *__restrict__ w) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t k = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < D; k += nw) {
+        const uint32_t c = __ldg(dc + k);
+        if (!nonuniform) {
+            if (lane == 0) w[k] = c - 2u;
+            continue;
+        }
+        const uint32_t u = __ldg(du + k), v = __ldg(de + k) >> 2;
+        uint32_t oa = __ldg(off + u), la = __ldg(off + u + 1) - 1u - oa;
+        uint32_t ob = __ldg(off + v), lb = __ldg(off + v + 1) - 1u - ob;
+        if (la > lb) {
+            uint32_t t = oa; oa = ob; ob = t;
+            t = la; la = lb; lb = t;
+        }
+        uint32_t hits = 0;
+        for (uint32_t i = lane; i < la; i += 32) {
+            const uint32_t x = __ldg(adj + oa + i) >> 2;
+            uint32_t lo = 0, hi = lb;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((__ldg(adj + ob + mid) >> 2) < x) lo = mid + 1;
+                else hi = mid;
+            }
+            hits += (lo < lb && (__ldg(adj + ob + lo) >> 2) == x);
+        }
+        hits = __reduce_add_sync(0xffffffffu, hits);
+        if (lane == 0) w[k] = c - hits - 2u;
+    }
+}
+
+// The queue loop itself is sequential (NsetSize resets at every cut), so one
+// warp walks the weights 32 at a time: an inclusive warp scan of the chunk
+// from the current start lane, the first lane whose running NsetSize
+// exceeds MaxNsetSize closes a queue, the scan restarts after it.
+// starts[q] = first dyad of queue q; out[0] = queues, out[1] = aggregate
+// NsetSize.
+__global__ void __launch_bounds__(32) k_queue_greedy(const uint32_t *__restrict__ w, uint64_t D,
+                                                     uint64_t max_nset, uint32_t *__restrict__ starts,
+                                                     unsigned long long *__restrict__ out) {
+    const uint32_t lane = threadIdx.x;
+    unsigned long long run = 0, total = 0, q = 0;
+    if (D > 0 && lane == 0) starts[0] = 0;
+    q = D > 0 ? 1 : 0;
+    for (uint64_t base = 0; base < D; base += 32) {
+        const bool valid = base + lane < D;
+        const unsigned long long x = valid ? __ldg(w + base + lane) : 0ull;
+        unsigned long long all = x;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) all += __shfl_xor_sync(0xffffffffu, all, o);
+        total += all;
+        uint32_t s = 0;                          // first lane of the open run
+        while (s < 32) {
+            unsigned long long p = lane >= s ? x : 0ull;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(0xffffffffu, p, o);
+                if (lane >= (uint32_t)o) p += y;
+            }
+            const uint32_t cross = __ballot_sync(0xffffffffu, valid && lane >= s && run + p > max_nset);
+            if (!cross) {
+                run += __shfl_sync(0xffffffffu, p, 31);
+                break;
+            }
+            const uint32_t c = __ffs(cross) - 1;   // this dyad closes the queue
+            const uint64_t next = base + c + 1;
+            if (next < D) {
+                if (lane == 0) starts[q] = (uint32_t)next;
+                q++;
+            }
+            run = 0;
+            s = c + 1;
+        }
+    }
+    if (lane == 0) {
+        out[0] = q;
+        out[1] = total;
+    }
+}
 }  // namespace
 
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
@@ -276,6 +374,55 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->bin_work[2] = hs[4];
         prof->bin_work[3] = hs[5];
         for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
+    }
+    return TC_OK;
+}
+
+tc_status task_queues_device(const tc_graph *g, int nonuniform, uint64_t max_nset, cudaStream_t s,
+                             uint64_t *starts, uint64_t cap, uint64_t *nq, uint64_t *total) {
+    const uint64_t D = g->st.dyads;
+    *nq = 0;
+    *total = 0;
+    if (D == 0) return TC_OK;
+    Mem mem = g->mem;
+    mem.stream = s;
+    tc_status st;
+    DevBuf<uint32_t> w, dst;
+    DevBuf<unsigned long long> out;
+    if ((st = w.allocate(mem, D)) != TC_OK) return st;
+    if ((st = dst.allocate(mem, D)) != TC_OK) return st;
+    if ((st = out.allocate(mem, 2)) != TC_OK) return st;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    k_queue_weights<<<(unsigned)sms * 8, 256, 0, s>>>(g->off, g->adj, g->dyad_u, g->dyad_e,
+                                                      g->dyad_c, D, nonuniform, w.p);
+    TC_CUDA(cudaGetLastError());
+    k_queue_greedy<<<1, 32, 0, s>>>(w.p, D, max_nset, dst.p, out.p);
+    TC_CUDA(cudaGetLastError());
+    unsigned long long h[2];
+    TC_CUDA(cudaMemcpyAsync(h, out.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    *nq = h[0];
+    *total = h[1];
+    if (h[0] > cap) {
+        set_error("%llu task queues exceed the capacity %llu", h[0], (unsigned long long)cap);
+        return TC_E_RANGE;
+    }
+    if (h[0]) {
+        uint32_t *tmp = (uint32_t *)malloc(h[0] * sizeof(uint32_t));
+        if (!tmp) {
+            set_error("host allocation failed");
+            return TC_E_OOM;
+        }
+        cudaError_t e = cudaMemcpyAsync(tmp, dst.p, h[0] * sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) {
+            free(tmp);
+            return cuda_status(e, "task queue copy");
+        }
+        for (uint64_t i = 0; i < h[0]; i++) starts[i] = tmp[i];
+        free(tmp);
     }
     return TC_OK;
 }

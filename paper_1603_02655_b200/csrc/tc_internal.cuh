@@ -119,6 +119,9 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
                               int mode64 = 0);  // a2-a4
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
                               uint64_t *bounds);                      // schedule.cu
+tc_status task_queues_device(const tc_graph *g, int nonuniform, uint64_t max_nset, cudaStream_t s,
+                             uint64_t *starts, uint64_t cap, uint64_t *nq,
+                             uint64_t *total);                        // schedule.cu (f3)
 
 // generic device-wide exclusive scan with a per-element input functor and an
 // output functor; scan.cuh
