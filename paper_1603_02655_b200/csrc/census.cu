@@ -160,6 +160,7 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     uint32_t t = d0;
     while (t < d1) {
         const uint32_t lim = min(d1, t + 15u);   // nibble counters hold 15
+#pragma unroll 2   // measured: 2 beats the default 4 (C3 thread bin 0.889 vs 0.899 ms) and 8
         for (; t < lim; t++) {
             const uint32_t kx = x | 3u, ky = y | 3u;
             const bool ta = kx <= ky;            // consume A (ties: A first)
@@ -270,12 +271,13 @@ __device__ __forceinline__ WarpDyad warp_dyad(const BinLists &L, const uint32_t 
 }
 
 // Thread-bin work is handed out dynamically: a block takes the next unit
-// (a quarter of a plan tile, kUnitDyads slots of one tile, in canonical tile
-// order) from a global cursor, so the kernel's tail is at most one unit per
+// (a half or a quarter of a plan tile's item slots, in canonical tile order)
+// from a global cursor, so the kernel's tail is at most one unit per
 // resident block instead of a static round-robin's extra tiles.
-constexpr uint32_t kUnitsPerTile = 4;
-constexpr uint32_t kUnitDyads = kPlanTile / kUnitsPerTile;
-static_assert(kUnitDyads % kCensusThreads == 0, "unit = whole block rounds");
+// Units per tile (host-chosen, launch_bins): halves when there are >= 4 tiles
+// per resident block (C3: 0.891 vs 0.899 ms), quarters otherwise (C2: 117
+// tiles for 740 blocks; halves cost 0.155 vs 0.13 ms there).
+static_assert(kPlanTile % (4 * kCensusThreads) == 0, "unit = whole block rounds");
 
 __device__ __forceinline__ uint64_t next_unit(unsigned long long *cursor, uint32_t *unit_s) {
     __syncthreads();   // every warp is done with the previous unit's unit_s
@@ -291,7 +293,7 @@ __device__ __forceinline__ uint64_t next_unit(unsigned long long *cursor, uint32
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
                 uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts,
-                unsigned long long *cursor) {
+                unsigned long long *cursor, uint32_t upt) {
     __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
     block_setup<false>(tab_s, wsh);
@@ -300,11 +302,12 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t unit_s;
-    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * kUnitsPerTile;
+    const uint32_t unit_dyads = kPlanTile / upt;
+    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * upt;
          unit = next_unit(cursor, &unit_s)) {
-        const uint64_t tile = unit / kUnitsPerTile;
-        const uint32_t part = (uint32_t)(unit % kUnitsPerTile) * kUnitDyads;
-        const uint32_t cnt = min(__ldg(tile_count + tile), part + kUnitDyads);
+        const uint64_t tile = unit / upt;
+        const uint32_t part = (uint32_t)(unit % upt) * unit_dyads;
+        const uint32_t cnt = min(__ldg(tile_count + tile), part + unit_dyads);
         const BinItemT *it = items + tile * kPlanTile;
         for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
@@ -455,17 +458,18 @@ __device__ __forceinline__ void block_finish64(Smem64 &S, Acc64 &c, unsigned lon
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_thread64(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
                   uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts,
-                  unsigned long long *cursor) {
+                  unsigned long long *cursor, uint32_t upt) {
     __shared__ Smem64 S;
     block_setup64(S);
     Acc64 c{{0, 0, 0}, 0};
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t unit_s;
-    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * kUnitsPerTile;
+    const uint32_t unit_dyads = kPlanTile / upt;
+    for (uint64_t unit = next_unit(cursor, &unit_s); unit < ntiles * upt;
          unit = next_unit(cursor, &unit_s)) {
-        const uint64_t tile = unit / kUnitsPerTile;
-        const uint32_t part = (uint32_t)(unit % kUnitsPerTile) * kUnitDyads;
-        const uint32_t cnt = min(__ldg(tile_count + tile), part + kUnitDyads);
+        const uint64_t tile = unit / upt;
+        const uint32_t part = (uint32_t)(unit % upt) * unit_dyads;
+        const uint32_t cnt = min(__ldg(tile_count + tile), part + unit_dyads);
         const BinItemT *it = items + tile * kPlanTile;
         for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
@@ -522,16 +526,17 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     else
         TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_census_thread,
                                                               kCensusThreads, 0));
-    const uint64_t units = bl.ntiles * kUnitsPerTile;
     uint64_t tgrid = (uint64_t)sms * (per > 0 ? per : 1);
+    const uint32_t upt = bl.ntiles >= 4 * tgrid ? 2u : 4u;   // units per plan tile
+    const uint64_t units = bl.ntiles * upt;
     if (tgrid > units) tgrid = units ? units : 1;
     if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
     if (mode64)
         k_census_thread64<<<(unsigned)tgrid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles,
-                                                                    g->adj, out, bl.cursor);
+                                                                    g->adj, out, bl.cursor, upt);
     else
         k_census_thread<<<(unsigned)tgrid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles,
-                                                                  g->adj, out, bl.cursor);
+                                                                  g->adj, out, bl.cursor, upt);
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
     if (mode64)
