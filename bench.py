@@ -35,6 +35,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
+from synth.device import DEVICE_CONFIGS, make_device_config  # noqa: E402
 
 METRIC = "triad-census arcs/sec at 1/2/4/8 B200 (Patents-shaped); % HBM roofline"
 UNIT = "arcs/s"
@@ -180,6 +181,11 @@ def run_reference(args):
     rank, _, world = env_rank()
     if rank != 0:
         return 0
+    if args.config in DEVICE_CONFIGS:
+        print(json.dumps({"impl": "reference", "unavailable": "config %s is drawn on the GPU "
+                          "(synth/device.py); the CPU oracle runs on host-drawn configs only"
+                          % args.config}), flush=True)
+        return 0
     a = synth.make_config(args.config)
     steps = max(args.steps, 1)
     per_step = max(2.0, min(8.0, 150.0 / (steps + args.warmup)))
@@ -206,10 +212,10 @@ def run_reference(args):
     return 0
 
 
-def config_of(a, stats):
+def config_of(a, stats, m_drawn=None):
     c = {"workload": "%s: %s" % (a.meta.get("config"), a.meta.get("label")),
          "generator": a.meta.get("generator"), "seed": a.meta.get("seed"), "n": a.n,
-         "m_drawn": a.m}
+         "m_drawn": a.m if m_drawn is None else m_drawn}
     if stats:
         c.update({"m": stats["m"], "dyads": stats["dyads"], "sum_deg_sq": stats["sum_deg_sq"],
                   "max_degree": stats["max_degree"]})
@@ -231,10 +237,17 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1603_02655_b200 as tcb
 
-    a = synth.make_config(args.config)
     dev = torch.device("cuda", local)
-    s_dev = torch.from_numpy(a.src.view(np.int32)).to(dev)
-    d_dev = torch.from_numpy(a.dst.view(np.int32)).to(dev)
+    if args.config in DEVICE_CONFIGS:
+        # too large for the host generator: drawn on the device (synth/device.py)
+        n_, s_dev, d_dev, meta_ = make_device_config(args.config, dev)
+        a = synth.Arcs(n_, None, None, meta_)
+        a_m = int(s_dev.numel())
+    else:
+        a = synth.make_config(args.config)
+        a_m = a.m
+        s_dev = torch.from_numpy(a.src.view(np.int32)).to(dev)
+        d_dev = torch.from_numpy(a.dst.view(np.int32)).to(dev)
     stream = torch.cuda.current_stream(dev)
     comm = tcb.comm_from_process_group(local) if world > 1 else None
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)  # > 126 MB L2
@@ -293,8 +306,14 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
 
     # e2e: host (pinned) arcs through the C ABI, H2D + D2H inside the region
-    s_host = torch.from_numpy(a.src.view(np.int32)).pin_memory()
-    d_host = torch.from_numpy(a.dst.view(np.int32)).pin_memory()
+    if a.src is None:
+        s_host = torch.empty(a_m, dtype=torch.int32, pin_memory=True)
+        d_host = torch.empty(a_m, dtype=torch.int32, pin_memory=True)
+        s_host.copy_(s_dev)
+        d_host.copy_(d_dev)
+    else:
+        s_host = torch.from_numpy(a.src.view(np.int32)).pin_memory()
+        d_host = torch.from_numpy(a.dst.view(np.int32)).pin_memory()
     s_np = s_host.numpy().view(np.uint32)
     d_np = d_host.numpy().view(np.uint32)
     one_step(s_np, d_np)          # warm
@@ -343,14 +362,14 @@ def run_ours(args):
     plan_ms = float(np.mean([p["plan_ms"] for p in profs]))
     build_ms = float(np.mean([p["build_ms"] for p in profs]))
     sum_all_bins_bytes = 4.0 * sum(bin_work) + 24.0 * sum(bin_dyads)
-    m_arcs = a.m
+    m_arcs = a_m
     line = {"metric": METRIC, "value": m_arcs * args.steps / (total_ms * 1e-3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": dict(config_of(a, stats), **{
+            "config": dict(config_of(a, stats, a_m), **{
                 "l2": "inputs > L2 (arcs %.0f MB, sort keys %.0f MB) and a 512 MB L2 flush "
-                      "before every timed step" % (8 * a.m / 1e6, 32 * a.m / 1e6),
+                      "before every timed step" % (8 * a_m / 1e6, 32 * a_m / 1e6),
                 "step": "a1 build from device arcs + a2 plan + a3/a4 kernels + a5 closing",
                 "census_mode": "64-type (f1)" if args.mode == "64" else "16-class",
                 "parallelism": "dp%d (replicated CSR, degree-balanced dyad shards, 1 NCCL "
@@ -368,11 +387,15 @@ def run_ours(args):
                          "peak_source": peak_src,
                          "all_bins_frac": (sum_all_bins_bytes / (sum(avg_k) * 1e-3) / 1e9) / hbm},
             "e2e": {"value": m_arcs * args.steps / (e2e_total * 1e-3), "unit": UNIT,
-                    "h2d_bytes_per_step": 8 * a.m, "d2h_bytes_per_step": 320},
+                    "h2d_bytes_per_step": 8 * a_m, "d2h_bytes_per_step": 320},
             "gpu_launches": launches_total,
             "clocks": clk.summary(),
             "census": [str(x) for x in ref_counts]}
-    if world == 1 and not args.no_cpu_baseline:
+    if world == 1 and not args.no_cpu_baseline and a.src is None:
+        line["cpu_baseline"] = None
+        line["cpu_baseline_note"] = ("device-generated config: the oracle would need the "
+                                     "1e9-arc graph on the host; see the C3 line")
+    elif world == 1 and not args.no_cpu_baseline:
         r = oracle_rate(a, args.cpu_seconds, steps=3)
         line["cpu_baseline"] = {
             "value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",

@@ -210,12 +210,17 @@ def tc_task_queues(g: Graph, strategy: str, max_nset_size: int, stream=None):
     NsetSize).  strategy: "uniform" or "nonuniform"."""
     strat = {"uniform": 0, "nonuniform": 1}[strategy]
     nq, tot = ctypes.c_uint64(0), ctypes.c_uint64(0)
-    cap = max(int(g.stats()["dyads"]), 1)     # never more queues than dyads
-    out = np.zeros(cap, np.uint64)
-    check(lib.tc_task_queues(g.handle, strat, int(max_nset_size), _stream_ptr(stream),
-                             out.ctypes.data_as(_lib.u64p), cap, ctypes.byref(nq),
-                             ctypes.byref(tot)), "tc_task_queues")
-    return out[:nq.value].copy(), int(tot.value)
+    cap = max(min(int(g.stats()["dyads"]), 1 << 16), 1)   # never more queues than dyads
+    while True:
+        out = np.zeros(cap, np.uint64)
+        st = lib.tc_task_queues(g.handle, strat, int(max_nset_size), _stream_ptr(stream),
+                                out.ctypes.data_as(_lib.u64p), cap, ctypes.byref(nq),
+                                ctypes.byref(tot))
+        if st == _lib.TC_E_RANGE and nq.value > cap:
+            cap = int(nq.value)                 # rerun with the exact count
+            continue
+        check(st, "tc_task_queues")
+        return out[:nq.value].copy(), int(tot.value)
 
 
 def tc_comm_unique_id() -> bytes:

@@ -49,3 +49,62 @@ def test_c4_sampled_ranges_vs_oracle(c4):
     for b, e in ranges:
         # classes 021D..300 per range exactly (012/102 move, reading 21)
         assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:], (b, e)
+
+
+# ---------------------------------------------------------------------------
+# C5 proxy: R-MAT scale 24, edge factor 16 (268M drawn arcs), drawn on the GPU
+# (synth/device.py).  Identities computed with plain torch ops from the arcs
+# (independent of the library), plus a cross-check of the triangle count
+# between two different GPU algorithms: the census's connected classes and
+# the task-queue intersection counts (f3: aggregate |S| = sum d^2 - 2D - 3T).
+# ---------------------------------------------------------------------------
+def torch_quantities(n, s, d):
+    import torch
+    s = s.long()
+    d = d.long()
+    keep = s != d
+    key = torch.unique(s[keep] * n + d[keep])
+    s, d = key // n, key % n
+    rk = d * n + s
+    pos = torch.searchsorted(key, rk).clamp(max=key.numel() - 1)
+    rev = key[pos] == rk
+    mut_arcs = int(rev.sum())
+    out = torch.bincount(s, minlength=n)
+    inn = torch.bincount(d, minlength=n)
+    mutb = torch.bincount(s[rev], minlength=n)
+    und = torch.unique(torch.minimum(s, d) * n + torch.maximum(s, d))
+    deg = torch.bincount(und // n, minlength=n) + torch.bincount(und % n, minlength=n)
+    return dict(n=n, M=mut_arcs // 2, A=int(key.numel()) - mut_arcs, D=int(und.numel()),
+                paths=int((out * inn - mutb).sum()), os=int((out * (out - 1) // 2).sum()),
+                is_=int((inn * (inn - 1) // 2).sum()), sumd2=int((deg * deg).sum()),
+                sumdc2=int((deg * (deg - 1) // 2).sum()))
+
+
+def test_c5_proxy_identities_and_triangles():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1603_02655_b200 as tcb
+    from synth.device import make_device_config
+    from test_oracle_identities import NAMES, _class_constants
+    n, s, d, meta = make_device_config("C5p", torch.device("cuda", 0))
+    q = torch_quantities(n, s, d)
+    g = tcb.tc_graph_create(n, s, d)
+    try:
+        del s, d
+        st = g.stats()
+        assert st["dyads"] == q["D"] and st["sum_deg_sq"] == q["sumd2"]
+        c = g.census()
+        check_identities(c, q)
+        # triangles from the f3 intersection kernel (a different GPU algorithm)
+        _, W = tcb.tc_task_queues(g, "nonuniform", 2**63)
+        T3 = q["sumd2"] - 2 * q["D"] - W
+        assert T3 % 3 == 0
+        T = T3 // 3
+        K = _class_constants()
+        cs = dict(zip(NAMES, c))
+        assert sum(cs[k] for k in NAMES if K[k]["conn"] == 3) == T
+        assert sum(cs[k] for k in NAMES if K[k]["conn"] == 2) == q["sumdc2"] - 3 * T
+        assert cs["012"] + cs["102"] == q["D"] * n - q["sumd2"] + 3 * T
+    finally:
+        g.close()
