@@ -63,6 +63,7 @@ struct DownSmem {
     uint32_t gbase[kMaxRadix];               // global offset - local offset per digit
 };
 
+template <int BITS>
 __global__ void __launch_bounds__(kDsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
              uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles) {
@@ -92,7 +93,7 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
         // (cheaper than __match_any_sync on sm_100)
         uint32_t peers = __ballot_sync(0xffffffffu, valid);
 #pragma unroll
-        for (int bit = 0; bit < kMaxBits; bit++) {
+        for (int bit = 0; bit < BITS; bit++) {   // only the digit's own bits
             const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
             peers &= ((d >> bit) & 1u) ? b : ~b;
         }
@@ -144,6 +145,9 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
     }
 }
 
+typedef void (*DownFn)(const uint64_t *, uint64_t *, size_t, int, uint32_t, int, const uint32_t *,
+                       size_t);
+
 }  // namespace
 
 tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
@@ -155,8 +159,12 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         set_error("radix sort: %zu keys exceed the 32-bit offset range", n);
         return TC_E_INVALID;
     }
-    TC_CUDA(cudaFuncSetAttribute(rs_downsweep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(DownSmem)));
+    static const DownFn kDown[kMaxBits + 1] = {nullptr,          rs_downsweep<1>, rs_downsweep<2>,
+                                               rs_downsweep<3>, rs_downsweep<4>, rs_downsweep<5>,
+                                               rs_downsweep<6>, rs_downsweep<7>, rs_downsweep<8>};
+    for (int b = 1; b <= kMaxBits; b++)
+        TC_CUDA(cudaFuncSetAttribute(kDown[b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)sizeof(DownSmem)));
     size_t ntiles = (n + kRsTile - 1) / kRsTile;
     int maxbits = 1;
     for (int p = 0; p < npasses; p++) maxbits = passes[p].bits > maxbits ? passes[p].bits : maxbits;
@@ -179,7 +187,7 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
                                       ArrayOutExcl<uint32_t>{hist.p}, (uint32_t *)nullptr, s,
                                       launches);
         if (st != TC_OK) return st;
-        rs_downsweep<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
+        kDown[bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
             src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles);
         TC_CUDA(cudaGetLastError());
         if (launches) *launches += 2;
