@@ -71,6 +71,11 @@ __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restr
     if ((threadIdx.x & 31) == 0 && loops) atomicAdd(&scratch[1], loops);
 }
 
+__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
 __device__ __forceinline__ uint32_t key_row(uint64_t k) { return (uint32_t)(k >> 32); }
 __device__ __forceinline__ uint32_t key_col(uint64_t k) { return (uint32_t)((k >> 2) & 0x3fffffffu); }
 __device__ __forceinline__ uint32_t swap_tag(uint32_t t) { return ((t & 1u) << 1) | (t >> 1); }
@@ -149,21 +154,6 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restr
     }
 }
 
-// start[x] = first index of row x in a row-sorted key array (rows with no
-// keys get the next row's start); the tail (rows after the last) is filled
-// by k_fill_tail
-__global__ void k_row_starts(const uint64_t *__restrict__ key, size_t L, uint32_t *start) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < L;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t row = key_row(__ldg(key + i));
-        const uint32_t prev = i ? key_row(__ldg(key + i - 1)) : 0xffffffffu;
-        if (i == 0 || prev != row) {
-            const uint32_t first = i == 0 ? 0u : prev + 1;
-            for (uint32_t x = first; x <= row; x++) start[x] = (uint32_t)i;
-        }
-    }
-}
-
 __global__ void k_fill_tail(uint32_t *start, uint64_t from, uint64_t n, uint32_t val) {
     for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
          x += (uint64_t)gridDim.x * blockDim.x)
@@ -176,9 +166,12 @@ __global__ void k_fill_tail(uint32_t *start, uint64_t from, uint64_t n, uint32_t
 // first entry w > u of row r: dyad_pb).  One random read-modify-write per
 // dyad into a D-word array (L2-resident at the Patents size) instead of a
 // search of row r.
+// The same pass records lo_start[x] = first index of row x among the
+// row-sorted transposed keys (rows with no lower entries get the next row's
+// start; the rows after the last one are filled by k_fill_tail_last).
 __global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
                               const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
-                              uint32_t *__restrict__ ul) {
+                              uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start) {
     for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < D;
          i += (size_t)gridDim.x * blockDim.x) {
         const uint64_t key = __ldg(tk + i);
@@ -186,46 +179,53 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
         const uint32_t pos = __ldg(up_start + r) + r + (uint32_t)i;
         adj[pos] = ul[k];
         ul[k] = pos + 1u;
+        const uint32_t prev = i ? key_row(__ldg(tk + i - 1)) : 0xffffffffu;
+        if (i == 0 || prev != r) {
+            const uint32_t first = i == 0 ? 0u : prev + 1;
+            for (uint32_t x = first; x <= r; x++) lo_start[x] = (uint32_t)i;
+        }
     }
+}
+
+// start[x] = val for x in (row of the last key, n]: the rows after the last
+// one of a row-sorted key array (read on the device: no host round trip)
+__global__ void k_fill_tail_last(uint32_t *start, const uint64_t *__restrict__ key, uint64_t L,
+                                 uint64_t n, uint32_t val) {
+    const uint64_t from = L ? (uint64_t)key_row(key[L - 1]) + 1 : 0;
+    for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        start[x] = val;
 }
 
 // off[u] = lo_start[u] + up_start[u] + u; sentinel at off[u+1] - 1; slack
 // after; ups[u] = off[u] + |lower part of u| = first entry w > u of row u
+// also the vertex stats: out[0] += sum d^2, out[1] = max d, d_u = |N(u)| =
+// (lo_start[u+1] - lo_start[u]) + (up_start[u+1] - up_start[u])
 __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
                           const uint32_t *__restrict__ up_start, uint64_t n,
                           uint32_t *__restrict__ off, uint32_t *__restrict__ ups,
-                          uint32_t *__restrict__ adj) {
+                          uint32_t *__restrict__ adj, unsigned long long *out) {
+    unsigned long long s2 = 0, mx = 0;
     for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n + 8;
          u += (uint64_t)gridDim.x * blockDim.x) {
         if (u <= n) {
             const uint32_t o = lo_start[u] + up_start[u] + (uint32_t)u;
             off[u] = o;
             if (u > 0) adj[o - 1] = 0xffffffffu;    // terminator of row u - 1
-            if (u < n) ups[u] = lo_start[u + 1] + up_start[u] + (uint32_t)u;
+            if (u < n) {
+                const uint32_t l1 = lo_start[u + 1], u1 = up_start[u + 1];
+                ups[u] = l1 + up_start[u] + (uint32_t)u;
+                const unsigned long long d = (l1 - lo_start[u]) + (u1 - up_start[u]);
+                s2 += d * d;
+                mx = d > mx ? d : mx;
+            }
         } else {
             adj[lo_start[n] + up_start[n] + (uint32_t)u - 1] = 0xffffffffu;   // slack
         }
     }
-}
-
-__device__ __forceinline__ unsigned long long warp_sum64(unsigned long long x) {
-    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    return x;
-}
-
-// [0] = sum d^2, [1] = max d
-__global__ void k_vertex_stats(const uint32_t *__restrict__ off, uint64_t n,
-                               unsigned long long *out) {
-    unsigned long long s2 = 0, mx = 0;
-    for (uint64_t u = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-         u += (uint64_t)gridDim.x * blockDim.x) {
-        unsigned long long d = off[u + 1] - off[u] - 1;
-        s2 += d * d;
-        mx = d > mx ? d : mx;
-    }
     s2 = warp_sum64(s2);
     for (int o = 16; o; o >>= 1) {
-        unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, mx, o);
         mx = y > mx ? y : mx;
     }
     if ((threadIdx.x & 31) == 0) {
@@ -233,6 +233,7 @@ __global__ void k_vertex_stats(const uint32_t *__restrict__ off, uint64_t n,
         atomicMax(&out[1], mx);
     }
 }
+
 
 // upper entries + per-dyad data, one thread per canonical dyad k = (u, v):
 // the entry of v goes to ups[u] + (k - up_start[u]) = lo_start[u+1] + u + k;
@@ -377,17 +378,8 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     if ((st = radix_sort_u64(mem, spare, tother, D, rpasses, nrp, s, &g->launches, &tsorted)) !=
         TC_OK)
         return st;
-    uint64_t tlast = 0;
-    if (D) {
-        k_row_starts<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, lo_start.p);
-        TC_CUDA(cudaMemcpyAsync(&tlast, tsorted + (D - 1), sizeof(uint64_t),
-                                cudaMemcpyDeviceToHost, s));
-        TC_CUDA(cudaStreamSynchronize(s));
-    }
-    const uint64_t lo_from = D ? ((tlast >> 32) + 1) : 0;
-    k_fill_tail<<<grid_for(n + 1 - lo_from, 256), 256, 0, s>>>(lo_start.p, lo_from, n, D);
-
-    // 5. assemble the symmetric rows
+    // 5. assemble the symmetric rows: lower entries (+ lo_start, dyad_pb),
+    // then offsets, sentinels and vertex stats, then upper entries
     const uint64_t nnz = 2ull * D;
     uint32_t *adj = (uint32_t *)mem.alloc((nnz + n + 8) * sizeof(uint32_t));
     g->adj = adj; g->adj_n = nnz + n + 8;
@@ -395,18 +387,20 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
-    k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj);
     if (D) {
-        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj, dpb);
+        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj, dpb,
+                                                       lo_start.p);
+        g->launches += 1;
+    }
+    k_fill_tail_last<<<grid_for(n + 1, 256), 256, 0, s>>>(lo_start.p, tsorted, D, n, D);
+    k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj,
+                                                   scratch.p + 4);
+    g->launches += 2;
+    if (D) {
         k_write_upper<<<grid_for(D, 256), 256, 0, s>>>(off, ups, lo_start.p, du, de, dpb, D, adj,
                                                        dc, dt, scratch.p + 4);
+        g->launches += 1;
     }
-    g->launches += D ? 3 : 1;
-    TC_CUDA(cudaGetLastError());
-
-    // 6. vertex stats
-    k_vertex_stats<<<grid_for(n, 256), 256, 0, s>>>(off, n, scratch.p + 4);
-    g->launches += 1;
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
