@@ -3,7 +3,8 @@
 //
 // One pass per digit of <= 8 bits (256 buckets), tiles of 4096 keys:
 //   upsweep    per-tile digit histogram (shared-memory atomics)
-//   scan       exclusive scan of the digit-major (digit, tile) histogram
+//   scan       per digit, exclusive scan over tiles + digit totals (one
+//              block per digit); the downsweep adds the digits' prefix
 //   downsweep  stable tile-local counting sort: per warp, one ballot per
 //              digit bit groups the lanes holding the same digit (__match_any
 //              is ~35% slower here) (rank = earlier peers
@@ -56,6 +57,35 @@ rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask
     for (int d = threadIdx.x; d < radix; d += kRsThreads) hist[(size_t)d * ntiles + blockIdx.x] = h[d];
 }
 
+// Digit-major histogram -> per-digit exclusive prefix over tiles, in place
+// (one block per digit, chunks of 4096 tiles with a running carry), and the
+// digit totals; the downsweep adds the exclusive prefix of the totals.  One
+// launch per pass instead of a device-wide reduce-then-scan pair.
+__global__ void __launch_bounds__(256) rs_scan_digits(uint32_t *__restrict__ hist, size_t ntiles,
+                                                      uint32_t *__restrict__ totals) {
+    uint32_t *row = hist + (size_t)blockIdx.x * ntiles;
+    uint32_t carry = 0;
+    for (size_t base = 0; base < ntiles; base += 256 * 16) {
+        uint32_t v[16], sum = 0;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const size_t i = base + (size_t)threadIdx.x * 16 + k;
+            v[k] = i < ntiles ? row[i] : 0u;
+            sum += v[k];
+        }
+        uint32_t all;
+        uint32_t run = block_exclusive_sum<uint32_t, 256>(sum, &all) + carry;
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const size_t i = base + (size_t)threadIdx.x * 16 + k;
+            if (i < ntiles) row[i] = run;
+            run += v[k];
+        }
+        carry += all;
+    }
+    if (threadIdx.x == 0) totals[blockIdx.x] = carry;
+}
+
 struct DownSmem {
     uint32_t klo[kRsTile], khi[kRsTile];     // tile reordered by digit (split halves:
                                              // 4-byte banks, fewer store conflicts)
@@ -66,7 +96,8 @@ struct DownSmem {
 template <int BITS>
 __global__ void __launch_bounds__(kDsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
-             uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles) {
+             uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles,
+             const uint32_t *__restrict__ totals) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     DownSmem &S = *reinterpret_cast<DownSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -114,10 +145,14 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
         uint32_t tot = 0;
         for (int d = d0; d < d0 + per && d < radix; d++)
             for (int w = 0; w < kDsWarps; w++) tot += S.wc[w][d];
+        uint32_t gt = 0;   // keys of the digits before mine, all tiles
+        for (int d = d0; d < d0 + per && d < radix; d++) gt += __ldg(totals + d);
         uint32_t all;
         uint32_t run = block_exclusive_sum<uint32_t, kDsThreads>(tot, &all);
+        uint32_t grun = block_exclusive_sum<uint32_t, kDsThreads>(gt, &all);
         for (int d = d0; d < d0 + per && d < radix; d++) {
-            S.gbase[d] = offs[(size_t)d * ntiles + blockIdx.x] - run;
+            S.gbase[d] = grun + offs[(size_t)d * ntiles + blockIdx.x] - run;
+            grun += __ldg(totals + d);
             for (int w = 0; w < kDsWarps; w++) {
                 uint32_t c = S.wc[w][d];
                 S.wc[w][d] = (uint16_t)run;
@@ -146,7 +181,7 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
 }
 
 typedef void (*DownFn)(const uint64_t *, uint64_t *, size_t, int, uint32_t, int, const uint32_t *,
-                       size_t);
+                       size_t, const uint32_t *);
 
 }  // namespace
 
@@ -168,9 +203,10 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
     size_t ntiles = (n + kRsTile - 1) / kRsTile;
     int maxbits = 1;
     for (int p = 0; p < npasses; p++) maxbits = passes[p].bits > maxbits ? passes[p].bits : maxbits;
-    DevBuf<uint32_t> hist;
+    DevBuf<uint32_t> hist, totals;
     tc_status st = hist.allocate(mem, ntiles << maxbits);
     if (st != TC_OK) return st;
+    if ((st = totals.allocate(mem, (size_t)1 << maxbits)) != TC_OK) return st;
     uint64_t *src = keys, *dst = tmp;
     for (int p = 0; p < npasses; p++) {
         int bits = passes[p].bits;
@@ -183,14 +219,12 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         rs_upsweep<<<(unsigned)ntiles, kRsThreads, 0, s>>>(src, n, passes[p].shift, mask, radix,
                                                            hist.p, ntiles);
         TC_CUDA(cudaGetLastError());
-        st = scan_exclusive<uint32_t>(mem, (size_t)radix * ntiles, ArrayIn<uint32_t>{hist.p},
-                                      ArrayOutExcl<uint32_t>{hist.p}, (uint32_t *)nullptr, s,
-                                      launches);
-        if (st != TC_OK) return st;
-        kDown[bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
-            src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles);
+        rs_scan_digits<<<(unsigned)radix, 256, 0, s>>>(hist.p, ntiles, totals.p);
         TC_CUDA(cudaGetLastError());
-        if (launches) *launches += 2;
+        kDown[bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
+            src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles, totals.p);
+        TC_CUDA(cudaGetLastError());
+        if (launches) *launches += 3;
         uint64_t *t = src;
         src = dst;
         dst = t;
