@@ -5,10 +5,11 @@
 // of P:458-469) where every entry carries the 2-bit direction code, so the
 // census never probes IsEdge / IsNeighbour -- the tags answer them.
 //
-//   1. emit      arc (s,d), s != d -> one canonical key (min<<32 | max<<2 |
-//                dir), dir = 1 if min->max else 2; self-loops -> all-ones
-//                sentinel keys that sort last (strict digraph);
-//                range check.
+//   1. keys      arc (s,d), s != d -> one canonical key (min<<32 | max<<2 |
+//                dir), dir = 1 if min->max else 2; self-loops and arcs with
+//                an endpoint >= n -> all-ones sentinel keys that sort last
+//                (strict digraph); computed by the first radix
+//                pass straight from the arc list, which also counts them.
 //   2. sort      LSD radix sort (radix_sort.cu) on the max bits, then the
 //                min bits: canonical pairs in the algorithm's own dyad order
 //                (u ascending, v ascending).
@@ -49,7 +50,7 @@ constexpr int kHcTile = kHcThreads * kHcItems;   // keys per block
 
 __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restrict__ dst,
                        uint64_t m, uint64_t n, uint64_t *__restrict__ keys,
-                       unsigned long long *__restrict__ scratch /* [0]=bad, [1]=loops */) {
+                       unsigned long long *__restrict__ scratch /* [0]=bad, [1]=dropped */) {
     unsigned long long loops = 0;
     for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -57,6 +58,7 @@ __global__ void k_emit(const uint32_t *__restrict__ src, const uint32_t *__restr
         uint64_t k;
         if (s >= n || d >= n) {
             atomicMin(&scratch[0], (unsigned long long)i);
+            loops++;                 // dropped-arc count: loops + out of range
             k = kSentinel;
         } else if (s == d) {
             loops++;
@@ -93,7 +95,9 @@ __device__ __forceinline__ void run_head(const uint64_t *__restrict__ key, size_
 
 // pass 1: per warp (512 keys), number of run heads
 __global__ void __launch_bounds__(kHcThreads)
-k_head_count(const uint64_t *__restrict__ key, size_t L, uint32_t *__restrict__ warp_tot) {
+k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
+             uint32_t *__restrict__ warp_tot) {
+    const size_t L = m - *dropped;   // canonical keys (dropped arcs sort last)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
     uint32_t nh = 0;
@@ -111,9 +115,11 @@ k_head_count(const uint64_t *__restrict__ key, size_t L, uint32_t *__restrict__ 
 // lower entry of each dyad (ul[k] = u<<2 | swapped tag) and up_start at row
 // changes (warp_off = exclusive scan of pass 1's per-warp counts)
 __global__ void __launch_bounds__(kHcThreads)
-k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restrict__ warp_off,
+k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
+             const uint32_t *__restrict__ warp_off,
              uint32_t *__restrict__ du, uint32_t *__restrict__ de, uint64_t *__restrict__ tk,
              uint32_t *__restrict__ ul, uint32_t *__restrict__ up_start) {
+    const size_t L = m - *dropped;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
@@ -154,11 +160,6 @@ k_head_write(const uint64_t *__restrict__ key, size_t L, const uint32_t *__restr
     }
 }
 
-__global__ void k_fill_tail(uint32_t *start, uint64_t from, uint64_t n, uint32_t val) {
-    for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
-         x += (uint64_t)gridDim.x * blockDim.x)
-        start[x] = val;
-}
 
 // lower entries: row r's i-th key of the row-sorted transposed list is dyad
 // k = (u, r); its entry ul[k] goes to off[r] + (i - lo_start[r]) =
@@ -185,6 +186,19 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
             for (uint32_t x = first; x <= r; x++) lo_start[x] = (uint32_t)i;
         }
     }
+}
+
+// up_start[x] = D for the rows after the last canonical row (L and D read
+// on the device)
+__global__ void k_fill_tail_up(uint32_t *start, const uint64_t *__restrict__ key, uint64_t m,
+                               const unsigned long long *dropped, uint64_t n,
+                               const uint32_t *__restrict__ total) {
+    const uint64_t L = m - *dropped;
+    const uint32_t D = *total;
+    const uint64_t from = (L && D) ? (uint64_t)key_row(key[L - 1]) + 1 : 0;
+    for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
+         x += (uint64_t)gridDim.x * blockDim.x)
+        start[x] = D;
 }
 
 // start[x] = val for x in (row of the last key, n]: the rows after the last
@@ -286,43 +300,39 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
     TC_CUDA(cudaMemcpyAsync(scratch.p, init, sizeof(init), cudaMemcpyHostToDevice, s));
 
+    if (2ull * m + n + 8 >= (1ull << 33)) {   // 2D + n < 2^32 is checked exactly below
+        set_error("%llu arcs: 2D + n can exceed the 32-bit CSR offset range",
+                  (unsigned long long)m);
+        return TC_E_INVALID;
+    }
     DevBuf<uint64_t> keys, tmp;
     if ((st = keys.allocate(mem, m)) != TC_OK) return st;
     if ((st = tmp.allocate(mem, m)) != TC_OK) return st;
-    if (m) {
-        k_emit<<<grid_for(m, 256), 256, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
-        g->launches++;
-        TC_CUDA(cudaGetLastError());
-    }
-    unsigned long long h[8];
-    TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    if (h[0] != ~0ull) {
-        set_error("arc %llu has an endpoint >= n (n = %llu)", h[0], (unsigned long long)n);
-        return TC_E_RANGE;
-    }
-    const uint64_t loops = h[1];
-    const size_t L = m - loops;                     // canonical keys before dedup
-    if (2ull * L + n + 8 >= (1ull << 32)) {
-        set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
-                  (unsigned long long)(2 * L + n));
-        return TC_E_INVALID;
-    }
 
-    // 2. sort canonical keys by (min, max): max bits first, then min bits
+    // 1 + 2. canonical keys by (min, max), sorted: max bits first, then min
+    // bits; the first radix pass computes the keys from the arcs itself and
+    // counts the dropped ones (no separate emit pass, no host round trip)
     int b = 1;
     while (b < 32 && (1ull << b) < n) b++;
     RadixPass passes[16];
     int np = radix_passes_for(2, b, passes);
     np += radix_passes_for(32, b, passes + np);
     uint64_t *sorted = keys.p;
-    if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted)) !=
-        TC_OK)
-        return st;
+    if (m >= 2) {
+        const ArcSource as{d_src, d_dst, n, scratch.p};
+        if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
+                                 &as)) != TC_OK)
+            return st;
+    } else if (m == 1) {
+        k_emit<<<1, 32, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
+        g->launches++;
+        TC_CUDA(cudaGetLastError());
+    }
     uint64_t *spare = sorted == keys.p ? tmp.p : keys.p;
 
-    // 3. compaction -> canonical dyads (upper halves) + transposed keys
-    const size_t cap = L ? L : 1;
+    // 3. compaction -> canonical dyads (upper halves) + transposed keys; the
+    // canonical key count L = m - dropped is read on the device
+    const size_t cap = m ? m : 1;
     uint32_t *du = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *de = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
     uint32_t *dc = (uint32_t *)mem.alloc(cap * sizeof(uint32_t));
@@ -345,30 +355,43 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     if ((st = up_start.allocate(mem, n + 1)) != TC_OK) return st;
     if ((st = lo_start.allocate(mem, n + 1)) != TC_OK) return st;
     uint32_t D = 0;
-    uint64_t lastkey = 0;
-    if (L) {
-        const size_t ntiles = (L + kHcTile - 1) / kHcTile;
-        DevBuf<uint32_t> wt, total;
+    DevBuf<uint32_t> total;
+    if ((st = total.allocate(mem, 1)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(total.p, 0, sizeof(uint32_t), s));
+    if (m) {
+        const size_t ntiles = (m + kHcTile - 1) / kHcTile;
+        DevBuf<uint32_t> wt;
         if ((st = wt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
-        if ((st = total.allocate(mem, 1)) != TC_OK) return st;
-        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p);
+        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p);
         TC_CUDA(cudaGetLastError());
         st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
                                       ArrayOutExcl<uint32_t>{wt.p}, total.p, s, &g->launches);
         if (st != TC_OK) return st;
-        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, L, wt.p, du, de, spare, dpb,
-                                                             up_start.p);
+        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p, du,
+                                                             de, spare, dpb, up_start.p);
         TC_CUDA(cudaGetLastError());
         g->launches += 2;
-        TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        TC_CUDA(cudaMemcpyAsync(&lastkey, sorted + (L - 1), sizeof(uint64_t),
-                                cudaMemcpyDeviceToHost, s));
-        TC_CUDA(cudaStreamSynchronize(s));
     }
     // rows after the last canonical row have no upper entries
-    const uint64_t up_from = D ? ((lastkey >> 32) + 1) : 0;
-    k_fill_tail<<<grid_for(n + 1 - up_from, 256), 256, 0, s>>>(up_start.p, up_from, n, D);
+    k_fill_tail_up<<<grid_for(n + 1, 256), 256, 0, s>>>(up_start.p, sorted, m, scratch.p + 1, n,
+                                                        total.p);
     TC_CUDA(cudaGetLastError());
+    // the one mid-build host read: range check, dropped arcs, D (sizes the
+    // transposed sort and the adjacency)
+    unsigned long long h[8];
+    TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
+    if (h[0] != ~0ull) {
+        set_error("arc %llu has an endpoint >= n (n = %llu)", h[0], (unsigned long long)n);
+        return TC_E_RANGE;
+    }
+    const uint64_t loops = h[1];
+    if (2ull * D + n + 8 >= (1ull << 32)) {
+        set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
+                  (unsigned long long)(2ull * D + n));
+        return TC_E_INVALID;
+    }
 
     // 4. lower halves: stable sort of the transposed keys on the row bits
     uint64_t *tsorted = spare;

@@ -28,14 +28,44 @@ constexpr int kDsItems = kRsTile / kDsThreads;
 constexpr int kMaxBits = 8;
 constexpr int kMaxRadix = 1 << kMaxBits;
 
+// The CSR builder's canonical key of arc (s, d) (csr_build.cu step 1):
+// min << 32 | max << 2 | dir, dir = 1 if min -> max else 2; self-loops and
+// arcs with an endpoint >= nv become all-ones keys that sort last.
+__device__ __forceinline__ uint64_t arc_key(uint32_t s, uint32_t d, uint64_t nv) {
+    if (s >= nv || d >= nv || s == d) return ~0ull;
+    const uint32_t lo = s < d ? s : d, hi = s < d ? d : s;
+    return ((uint64_t)lo << 32) | ((uint64_t)hi << 2) | (s < d ? 1ull : 2ull);
+}
+
+// ARCS: the first pass reads the arc list itself (no separate key-emit pass)
+// and counts the dropped arcs: a.scratch[1] += loops + out-of-range arcs,
+// a.scratch[0] = min index of an out-of-range arc.
+template <bool ARCS>
 __global__ void __launch_bounds__(kRsThreads)
 rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask, int radix,
-           uint32_t *__restrict__ hist, size_t ntiles) {
+           uint32_t *__restrict__ hist, size_t ntiles, ArcSource a) {
     __shared__ uint32_t h[kMaxRadix];
     for (int i = threadIdx.x; i < radix; i += kRsThreads) h[i] = 0;
     __syncthreads();
     const size_t base = (size_t)blockIdx.x * kRsTile;
-    if (base + kRsTile <= n) {
+    if (ARCS) {
+        unsigned long long dropped = 0;
+#pragma unroll 4
+        for (int k = 0; k < kRsItems; k++) {
+            const size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
+            if (i < n) {
+                const uint32_t sv = __ldg(a.src + i), dv = __ldg(a.dst + i);
+                const uint64_t key = arc_key(sv, dv, a.nv);
+                if (key == ~0ull) {
+                    dropped++;
+                    if (sv >= a.nv || dv >= a.nv) atomicMin(&a.scratch[0], (unsigned long long)i);
+                }
+                atomicAdd(&h[(uint32_t)(key >> shift) & mask], 1u);
+            }
+        }
+        for (int o = 16; o; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);
+        if ((threadIdx.x & 31) == 0 && dropped) atomicAdd(&a.scratch[1], dropped);
+    } else if (base + kRsTile <= n) {
         // full tile: all 16 keys in flight as 8 x 16-byte loads, then count
         const ulonglong2 *k2 = reinterpret_cast<const ulonglong2 *>(keys + base);
         ulonglong2 v[kRsItems / 2];
@@ -93,11 +123,11 @@ struct DownSmem {
     uint32_t gbase[kMaxRadix];               // global offset - local offset per digit
 };
 
-template <int BITS>
+template <int BITS, bool ARCS>
 __global__ void __launch_bounds__(kDsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
              uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles,
-             const uint32_t *__restrict__ totals) {
+             const uint32_t *__restrict__ totals, ArcSource a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     DownSmem &S = *reinterpret_cast<DownSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -113,7 +143,8 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
 #pragma unroll
     for (int k = 0; k < kDsItems; k++) {
         size_t i = wbase + (size_t)k * 32 + lane;
-        key[k] = i < n ? __ldcs(keys + i) : 0ull;
+        if (ARCS) key[k] = i < n ? arc_key(__ldcs(a.src + i), __ldcs(a.dst + i), a.nv) : 0ull;
+        else key[k] = i < n ? __ldcs(keys + i) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < kDsItems; k++) {
@@ -181,25 +212,32 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
 }
 
 typedef void (*DownFn)(const uint64_t *, uint64_t *, size_t, int, uint32_t, int, const uint32_t *,
-                       size_t, const uint32_t *);
+                       size_t, const uint32_t *, ArcSource);
+#define TC_DS(A) {nullptr, rs_downsweep<1, A>, rs_downsweep<2, A>, rs_downsweep<3, A>,       \
+                  rs_downsweep<4, A>, rs_downsweep<5, A>, rs_downsweep<6, A>,            \
+                  rs_downsweep<7, A>, rs_downsweep<8, A>}
 
 }  // namespace
 
 tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
                          const RadixPass *passes, int npasses, cudaStream_t s,
-                         uint64_t *launches, uint64_t **sorted) {
+                         uint64_t *launches, uint64_t **sorted, const ArcSource *arcs) {
     *sorted = keys;
     if (n <= 1 || npasses == 0) return TC_OK;
     if (n >= (1ull << 32)) {
         set_error("radix sort: %zu keys exceed the 32-bit offset range", n);
         return TC_E_INVALID;
     }
-    static const DownFn kDown[kMaxBits + 1] = {nullptr,          rs_downsweep<1>, rs_downsweep<2>,
-                                               rs_downsweep<3>, rs_downsweep<4>, rs_downsweep<5>,
-                                               rs_downsweep<6>, rs_downsweep<7>, rs_downsweep<8>};
-    for (int b = 1; b <= kMaxBits; b++)
-        TC_CUDA(cudaFuncSetAttribute(kDown[b], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)sizeof(DownSmem)));
+    if (arcs && npasses == 0) {
+        set_error("radix sort: an arc source needs at least one pass");
+        return TC_E_INVALID;
+    }
+    static const DownFn kDown[2][kMaxBits + 1] = {TC_DS(false), TC_DS(true)};
+    for (int a = 0; a < 2; a++)
+        for (int b = 1; b <= kMaxBits; b++)
+            TC_CUDA(cudaFuncSetAttribute(kDown[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sizeof(DownSmem)));
+    const ArcSource none{nullptr, nullptr, 0, nullptr};
     size_t ntiles = (n + kRsTile - 1) / kRsTile;
     int maxbits = 1;
     for (int p = 0; p < npasses; p++) maxbits = passes[p].bits > maxbits ? passes[p].bits : maxbits;
@@ -216,13 +254,19 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         }
         int radix = 1 << bits;
         uint32_t mask = (uint32_t)radix - 1u;
-        rs_upsweep<<<(unsigned)ntiles, kRsThreads, 0, s>>>(src, n, passes[p].shift, mask, radix,
-                                                           hist.p, ntiles);
+        const bool from_arcs = arcs && p == 0;
+        if (from_arcs)
+            rs_upsweep<true><<<(unsigned)ntiles, kRsThreads, 0, s>>>(
+                src, n, passes[p].shift, mask, radix, hist.p, ntiles, *arcs);
+        else
+            rs_upsweep<false><<<(unsigned)ntiles, kRsThreads, 0, s>>>(
+                src, n, passes[p].shift, mask, radix, hist.p, ntiles, none);
         TC_CUDA(cudaGetLastError());
         rs_scan_digits<<<(unsigned)radix, 256, 0, s>>>(hist.p, ntiles, totals.p);
         TC_CUDA(cudaGetLastError());
-        kDown[bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
-            src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles, totals.p);
+        kDown[from_arcs][bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
+            src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles, totals.p,
+            from_arcs ? *arcs : none);
         TC_CUDA(cudaGetLastError());
         if (launches) *launches += 3;
         uint64_t *t = src;
