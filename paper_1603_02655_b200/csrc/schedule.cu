@@ -101,7 +101,11 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         }
     }
     __syncthreads();
-    extern __shared__ uint4 stage[];   // the tile's thread list, staged for coalesced stores
+    // the tile's thread list as a permutation (sorted slot -> tile index):
+    // 8 KB of shared memory instead of 64 KB of staged 16-byte items, so 5
+    // blocks fit per SM (0.27 vs 0.34 ms at C3); the items are gathered from
+    // the tile's dyad arrays (L1/L2-resident) and stored coalesced at the end
+    __shared__ uint16_t perm[kPlanTile];
     unsigned long long wt = 0, ww = 0, tt = 0, tw = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
 #pragma unroll 4
     for (int k = 0; k < kPlanItems; k++) {
@@ -110,14 +114,14 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         const uint32_t c = cst[k], d = digit_of(c);
         uint32_t nch = 0;
         if (valid) {
-            const uint32_t u = __ldg(P.du + i), e = __ldg(P.de + i), pre = e & 3u;
+            const uint32_t e = __ldg(P.de + i), pre = e & 3u;
             const uint32_t cf = __ldg(P.dc + i);
             const unsigned long long dy = n - cf;
             dy1 += pre == 1u ? dy : 0ull;
             dy2 += pre == 2u ? dy : 0ull;
             dy3 += pre == 3u ? dy : 0ull;
             if (d < 255u) {
-                stage[wc[warp][d] + rank[k]] = make_uint4(__ldg(P.ups + u), __ldg(P.dpb + i), e, c);
+                perm[wc[warp][d] + rank[k]] = (uint16_t)(wbase + k * 32 + lane);
                 wt += cf;
                 tt += c;
             } else {
@@ -147,7 +151,11 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     }
     __syncthreads();
     uint4 *out = reinterpret_cast<uint4 *>(tl + tile0);
-    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) out[j] = stage[j];
+    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) {
+        const uint64_t i = tile0 + perm[j];
+        const uint32_t u = __ldg(P.du + i);
+        out[j] = make_uint4(__ldg(P.ups + u), __ldg(P.dpb + i), __ldg(P.de + i), __ldg(P.dt + i));
+    }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
         wt += __shfl_xor_sync(0xffffffffu, wt, o);
@@ -328,10 +336,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     TC_CUDA(cudaMemsetAsync(stats.p, 0, 8 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off};
-    const int stage_bytes = kPlanTile * (int)sizeof(BinItemT);
-    TC_CUDA(cudaFuncSetAttribute(k_plan_tile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 stage_bytes));
-    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, stage_bytes, s>>>(
+    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
         P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
         reinterpret_cast<unsigned long long *>(d_counts), mode64);
     TC_CUDA(cudaGetLastError());
