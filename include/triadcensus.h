@@ -212,6 +212,16 @@ tc_status tc_task_queues(const tc_graph *g, int strategy, uint64_t max_nset_size
  * loaded if present); TC_E_NCCL if unavailable. */
 tc_status tc_comm_unique_id(uint8_t id[128]);
 tc_status tc_comm_create(const uint8_t id[128], int world, int rank, int device, tc_comm **out);
+
+/* Optional alternative bootstrap: borrow an
+ * existing ncclComm_t, e.g. torch's own through the private
+ * ProcessGroupNCCL._comm_ptr().  Valid only because the library dlopens the
+ * libnccl.so.2 already loaded into the process (torch's copy): the handle
+ * must come from that same library.  World size, rank and device are read
+ * from the communicator (ncclCommCount / UserRank / CuDevice).  The caller
+ * keeps ownership: tc_comm_destroy frees only the wrapper.  Errors:
+ * TC_E_INVALID (NULL), TC_E_NCCL (library or query failure). */
+tc_status tc_comm_wrap(void *borrowed_nccl_comm, tc_comm **out);
 void tc_comm_destroy(tc_comm *c);
 
 /* Multi-GPU census: each rank holds the full graph (replicated CSR),

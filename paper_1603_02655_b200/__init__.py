@@ -25,7 +25,8 @@ CLASS_NAMES = ("003", "012", "102", "021D", "021U", "021C", "111D", "111U",
 
 __all__ = ["tc_read_arcs", "census_file", "CLASS_NAMES", "Graph", "TCError", "tc_graph_create", "tc_census", "tc_census_range",
            "tc_census_enqueue", "tc_census_multi", "tc_census64", "tc_close_census", "tc_shard_bounds",
-           "tc_shard_bounds_host", "tc_comm_create", "tc_comm_unique_id", "Comm",
+           "tc_shard_bounds_host", "tc_comm_create", "tc_comm_unique_id", "tc_comm_wrap",
+           "comm_from_process_group", "comm_wrap_process_group", "tc_task_queues", "Comm",
            "census", "lib"]
 
 
@@ -265,6 +266,28 @@ def comm_from_process_group(device: int, group=None) -> Comm:
     obj = [tc_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     return tc_comm_create(obj[0], world, rank, device)
+
+
+def tc_comm_wrap(nccl_comm_ptr: int) -> Comm:
+    """Wrap a borrowed ncclComm_t (not owned; see include/triadcensus.h)."""
+    h = ctypes.c_void_p()
+    check(lib.tc_comm_wrap(ctypes.c_void_p(int(nccl_comm_ptr)), ctypes.byref(h)), "tc_comm_wrap")
+    return Comm(h.value)
+
+
+def comm_wrap_process_group(device: int, group=None) -> Comm:
+    """Borrow torch's own NCCL communicator of an initialised NCCL process
+    group (private API ProcessGroupNCCL._comm_ptr(); version-coupled, so
+    comm_from_process_group stays the default)."""
+    import torch
+    import torch.distributed as dist
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    dev = torch.device("cuda", device)
+    backend = pg._get_backend(dev)
+    # make sure torch has created the communicator for this device
+    t = torch.zeros(1, device=dev)
+    dist.all_reduce(t, group=group)
+    return tc_comm_wrap(backend._comm_ptr())
 
 
 def tc_census_multi(g: Graph, comm: Comm, stream=None) -> list[int]:

@@ -67,6 +67,7 @@ _SIGS = {
     "tc_comm_unique_id": (cint, [ctypes.POINTER(ctypes.c_uint8)]),
     "tc_comm_create": (cint, [ctypes.POINTER(ctypes.c_uint8), cint, cint, cint, ctypes.POINTER(vp)]),
     "tc_comm_destroy": (None, [vp]),
+    "tc_comm_wrap": (cint, [vp, ctypes.POINTER(vp)]),
     "tc_census_multi": (cint, [vp, vp, vp, u64p, u64p]),
     "tc_profile_enable": (cint, [vp, cint]),
     "tc_profile_get": (cint, [vp, ctypes.POINTER(tc_profile)]),

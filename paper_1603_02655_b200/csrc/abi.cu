@@ -370,6 +370,7 @@ typedef int (*fn_init_rank)(nccl_comm_t *, int, nccl_uid, int);
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, nccl_comm_t, cudaStream_t);
 typedef int (*fn_destroy)(nccl_comm_t);
 typedef const char *(*fn_errstr)(int);
+typedef int (*fn_comm_int)(nccl_comm_t, int *);
 
 struct Nccl {
     void *h = nullptr;
@@ -378,6 +379,7 @@ struct Nccl {
     fn_allreduce allreduce = nullptr;
     fn_destroy destroy = nullptr;
     fn_errstr errstr = nullptr;
+    fn_comm_int count = nullptr, user_rank = nullptr, cu_device = nullptr;
 };
 
 Nccl *nccl() {
@@ -397,6 +399,9 @@ Nccl *nccl() {
     n.allreduce = (fn_allreduce)dlsym(n.h, "ncclAllReduce");
     n.destroy = (fn_destroy)dlsym(n.h, "ncclCommDestroy");
     n.errstr = (fn_errstr)dlsym(n.h, "ncclGetErrorString");
+    n.count = (fn_comm_int)dlsym(n.h, "ncclCommCount");
+    n.user_rank = (fn_comm_int)dlsym(n.h, "ncclCommUserRank");
+    n.cu_device = (fn_comm_int)dlsym(n.h, "ncclCommCuDevice");
     if (!n.get_uid || !n.init_rank || !n.allreduce || !n.destroy) {
         n.h = nullptr;
         return nullptr;
@@ -417,6 +422,7 @@ tc_status nccl_fail(Nccl *n, int rc, const char *what) {
 struct tc_comm {
     nccl_comm_t comm = nullptr;
     int world = 1, rank = 0, device = 0;
+    bool borrowed = false;   // tc_comm_wrap: the caller owns the ncclComm_t
 };
 
 extern "C" {
@@ -460,10 +466,35 @@ tc_status tc_comm_create(const uint8_t id[128], int world, int rank, int device,
     return TC_OK;
 }
 
+tc_status tc_comm_wrap(void *borrowed_nccl_comm, tc_comm **out) {
+    if (!borrowed_nccl_comm || !out) {
+        set_error("invalid communicator arguments");
+        return TC_E_INVALID;
+    }
+    Nccl *n = nccl();
+    if (!n || !n->count || !n->user_rank || !n->cu_device) {
+        set_error("libnccl.so.2 (with ncclCommCount/UserRank/CuDevice) could not be loaded");
+        return TC_E_NCCL;
+    }
+    nccl_comm_t cm = (nccl_comm_t)borrowed_nccl_comm;
+    int world = 0, rank = 0, dev = 0, rc;
+    if ((rc = n->count(cm, &world))) return nccl_fail(n, rc, "ncclCommCount");
+    if ((rc = n->user_rank(cm, &rank))) return nccl_fail(n, rc, "ncclCommUserRank");
+    if ((rc = n->cu_device(cm, &dev))) return nccl_fail(n, rc, "ncclCommCuDevice");
+    tc_comm *c = new tc_comm();
+    c->comm = cm;
+    c->world = world;
+    c->rank = rank;
+    c->device = dev;
+    c->borrowed = true;
+    *out = c;
+    return TC_OK;
+}
+
 void tc_comm_destroy(tc_comm *c) {
     if (!c) return;
     Nccl *n = nccl();
-    if (n && c->comm) n->destroy(c->comm);
+    if (n && c->comm && !c->borrowed) n->destroy(c->comm);
     delete c;
 }
 

@@ -266,6 +266,28 @@ def test_census_multi_world1_nccl(tcb):
         g.close()
 
 
+def test_census_multi_world1_borrowed_torch_comm(tcb):
+    # tc_comm_wrap: torch's own NCCL communicator (1-rank group), borrowed
+    import socket
+    import torch.distributed as dist
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    dist.init_process_group("nccl", init_method="tcp://127.0.0.1:%d" % port, rank=0,
+                            world_size=1)
+    a = synth.make_config("C2")
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    try:
+        comm = tcb.comm_wrap_process_group(0)
+        try:
+            assert tcb.tc_census_multi(g, comm) == g.census()
+        finally:
+            comm.close()          # frees the wrapper only; torch keeps its comm
+    finally:
+        g.close()
+        dist.destroy_process_group()
+
+
 def test_census64_vs_oracle(tcb):
     # f1: 64-type census, GPU vs oracle element by element
     cases = [synth.random_digraph(n, p, seed=7000 + n, loops=True, dups=3)
