@@ -46,10 +46,6 @@
 // blocks end with one global atomicAdd per class.
 #include "census.cuh"
 
-#ifndef TC_AHEAD
-#define TC_AHEAD 0
-#endif
-
 namespace tc {
 
 // TriadTable, 0-based classes in the paper's order 003..300.
@@ -313,33 +309,6 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
         const uint32_t part = (uint32_t)(unit % upt) * unit_dyads;
         const uint32_t cnt = min(__ldg(tile_count + tile), part + unit_dyads);
         const BinItemT *it = items + tile * kPlanTile;
-#if TC_AHEAD
-        // one chunk of look-ahead: the next chunk's item is loaded and its
-        // rows prefetched into L2 before this chunk's merges start
-        uint32_t base = part + warp * 32;
-        bool valid = base + lane < cnt;
-        BinItemT e{0, 0, 0, 0};
-        if (valid) {
-            e = it[base + lane];
-            prefetch_row_l2(adj, e.pa, e.t);
-            prefetch_row_l2(adj, e.pb, e.t);
-        }
-        while (base < cnt) {
-            const uint32_t nb = base + kCensusThreads;
-            const bool nvalid = nb + lane < cnt;
-            BinItemT nx{0, 0, 0, 0};
-            if (nvalid) {
-                nx = it[nb + lane];
-                prefetch_row_l2(adj, nx.pa, nx.t);
-                prefetch_row_l2(adj, nx.pb, nx.t);
-            }
-            warp_reserve(c, wsh[warp], e.t);
-            if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
-            e = nx;
-            valid = nvalid;
-            base = nb;
-        }
-#else
         for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
             BinItemT e{0, 0, 0, 0};
@@ -353,7 +322,6 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
             warp_reserve(c, wsh[warp], e.t);
             if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
         }
-#endif
     }
     block_finish(c, wsh, d_counts);
 }
