@@ -197,6 +197,7 @@ void tc_graph_destroy(tc_graph *g) {
     g->mem.free(g->dyad_pb, g->dyad_n * 4);
     g->mem.free(g->dyad_t, g->dyad_n * 4);
     g->mem.free(g->ups, g->ups_n * 4);
+    if (g->tagpre) g->mem.free(g->tagpre, g->tagpre_n * 8);
     cudaStreamSynchronize(g->stream);
     delete g;
 }

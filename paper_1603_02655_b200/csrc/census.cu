@@ -334,8 +334,119 @@ __device__ __forceinline__ uint64_t next_item(unsigned long long *cursor) {
     return __shfl_sync(0xffffffffu, it, 0);
 }
 
+// ---------------------------------------------------------------------------
+// Skewed-pair items (schedule.cu sparse_mode): instead of merging a short
+// list with a long one, every entry of the short list is looked up in the
+// long list by binary search, and the long list's own contribution is read
+// from the tag prefix counts.  The same canonical triads are counted as by
+// the merge (census.cu header):
+//   mode 1, iterate A (entries w > u of N(u)), search B (entries > u of
+//   N(v)): w > v -> class T[pre | tu<<2 | tv<<4]; an intersection element
+//   (tv != 0) adds own I and, for w > v, the owed dyadic triad; B-only
+//   elements are all canonical with T[pre | tv<<4]: item chunk 0 adds every B
+//   entry by tag, each intersection element found takes its one back.
+//   mode 2, iterate B, search A: tu == 0 -> T[pre | tv<<4]; an intersection
+//   element adds own I and, for w > v, T[pre | tu<<2 | tv<<4] + the owed
+//   dyadic triad; A-only elements w > v are canonical with T[pre | tu<<2]:
+//   chunk 0 adds every A entry after v by tag, each intersection w > v
+//   takes its one back.
+// Class counts go to block shared u64 counters (wrapping adds: a take-back
+// may run ahead of its chunk-0 add; the totals are exact).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lower_id(const uint32_t *__restrict__ L, uint32_t len,
+                                             uint32_t x) {
+    uint32_t lo = 0, hi = len;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if ((__ldg(L + mid) >> 2) < x) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t tag_in(const uint32_t *__restrict__ L, uint32_t len,
+                                           uint32_t x) {
+    const uint32_t p = lower_id(L, len, x);
+    if (p < len) {
+        const uint32_t e = __ldg(L + p);
+        if ((e >> 2) == x) return e & 3u;
+    }
+    return 0u;
+}
+
+__device__ __forceinline__ void sp_add(unsigned long long *sp, uint32_t cls,
+                                       unsigned long long x) {
+    atomicAdd(&sp[cls], x);
+}
+
+__device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__restrict__ P,
+                            const WarpDyad &w, uint32_t mode, uint32_t d0, uint32_t d1,
+                            unsigned long long *sp) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t v = w.e >> 2, pre = w.e & 3u;
+    const unsigned long long minus1 = ~0ull;
+    uint32_t own = 0, o012 = 0, o102 = 0;
+    if (mode == 1u) {
+        for (uint32_t j = d0 + lane; j < d1; j += 32) {
+            const uint32_t x = __ldg(adj + w.oa + j), id = x >> 2, tu = x & 3u;
+            if (id == v) continue;
+            const uint32_t tv = tag_in(adj + w.ob, w.b, id);
+            if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1ull);
+            if (tv) {
+                own++;
+                if (id > v) {
+                    o102 += tv == 3u;
+                    o012 += tv != 3u;
+                }
+                sp_add(sp, c_triad_table[pre | tv << 4], minus1);
+            }
+        }
+        if (d0 == 0 && lane == 0) {
+            const uint64_t dd = __ldg(P + w.ob + w.b) - __ldg(P + w.ob);
+            const uint32_t c1 = (uint32_t)(dd >> 32), c2 = (uint32_t)dd;
+            const uint32_t cnt[4] = {0u, c1, c2, w.b - c1 - c2};
+            for (uint32_t t = 1; t <= 3; t++)
+                if (cnt[t]) sp_add(sp, c_triad_table[pre | t << 4], cnt[t]);
+        }
+    } else {
+        for (uint32_t j = d0 + lane; j < d1; j += 32) {
+            const uint32_t y = __ldg(adj + w.ob + j), id = y >> 2, tv = y & 3u;
+            const uint32_t tu = tag_in(adj + w.oa, w.a, id);
+            if (!tu) {
+                sp_add(sp, c_triad_table[pre | tv << 4], 1ull);
+            } else {
+                own++;
+                if (id > v) {
+                    sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1ull);
+                    o102 += tv == 3u;
+                    o012 += tv != 3u;
+                    sp_add(sp, c_triad_table[pre | tu << 2], minus1);
+                }
+            }
+        }
+        if (d0 == 0 && lane == 0) {
+            const uint32_t pv = lower_id(adj + w.oa, w.a, v) + 1u;   // entries after v
+            const uint64_t dd = __ldg(P + w.oa + w.a) - __ldg(P + w.oa + pv);
+            const uint32_t c1 = (uint32_t)(dd >> 32), c2 = (uint32_t)dd;
+            const uint32_t cnt[4] = {0u, c1, c2, (w.a - pv) - c1 - c2};
+            for (uint32_t t = 1; t <= 3; t++)
+                if (cnt[t]) sp_add(sp, c_triad_table[pre | t << 2], cnt[t]);
+        }
+    }
+    // own I -> the dyad's dyadic class; owed dyadic triads by tv
+    own = __reduce_add_sync(0xffffffffu, own);
+    o012 = __reduce_add_sync(0xffffffffu, o012);
+    o102 = __reduce_add_sync(0xffffffffu, o102);
+    if (lane == 0) {
+        if (own) sp_add(sp, pre == 3u ? 2u : 1u, own);
+        if (o012) sp_add(sp, 1u, o012);
+        if (o102) sp_add(sp, 2u, o102);
+    }
+}
+
 // warp bin: one warp per item = one dyad's diagonals [d0, d1), 32 lane
-// segments of <= kLaneSpan diagonals each
+// segments of <= kLaneSpan diagonals each; or a skewed-pair item (pad =
+// mode) = short-list entries [d0, d1)
 __global__ void __launch_bounds__(kCensusThreads)
 k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
               const uint32_t *__restrict__ adj, unsigned long long *d_counts) {
@@ -346,16 +457,25 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
     Acc c;
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ unsigned long long sp[16];   // skewed-pair class counts (wrapping)
+    if (threadIdx.x < 16) sp[threadIdx.x] = 0;
+    __syncthreads();
     const uint64_t count = *L.w_count;
     for (uint64_t it = next_item(L.wcursor); it < count; it = next_item(L.wcursor)) {
         const BinItemW e = L.w[it];
         const WarpDyad w = warp_dyad(L, off, ups, e.k);
+        if (e.pad) {   // warp-uniform
+            sparse_item(adj, L.tagpre, w, e.pad, e.d0, e.d1, sp);
+            continue;
+        }
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
         const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
         warp_reserve(c, wsh[warp], d1 - d0);
         if (d0 < d1) merge_diag<true>(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
     }
     block_finish(c, wsh, d_counts);
+    if (threadIdx.x >= 1 && threadIdx.x < 16 && sp[threadIdx.x])
+        atomicAdd(&d_counts[threadIdx.x], sp[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------

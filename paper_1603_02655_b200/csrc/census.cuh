@@ -15,6 +15,7 @@ struct BinLists {
     unsigned long long *cursor = nullptr;   // device, zeroed: thread-bin unit dispatch cursor
     unsigned long long *wcursor = nullptr;  // device, zeroed: warp-bin item dispatch cursor
     const uint32_t *du = nullptr, *de = nullptr, *dpb = nullptr;   // dyad arrays of the range
+    const uint64_t *tagpre = nullptr;       // tag prefix counts (skewed-pair items) or null
 };
 
 constexpr int kCensusThreads = 256;

@@ -280,6 +280,15 @@ __global__ void k_write_upper(const uint32_t *__restrict__ off, const uint32_t *
     }
 }
 
+// (tag == 1) << 32 | (tag == 2) of adj entry i (sentinels count as tag 3)
+struct TagIn {
+    const uint32_t *adj;
+    __device__ __forceinline__ uint64_t operator()(size_t i) const {
+        const uint32_t t = __ldg(adj + i) & 3u;
+        return (t == 1u ? (1ull << 32) : 0ull) | (t == 2u ? 1ull : 0ull);
+    }
+};
+
 inline unsigned grid_for(uint64_t work, int threads, int cap = 148 * 16) {
     uint64_t b = (work + threads - 1) / threads;
     if (b < 1) b = 1;
@@ -427,6 +436,21 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
+    // 7. tag prefix counts for the skewed-pair path (hub graphs only)
+    if (h[5] >= kSparseMinDegree) {
+        const size_t nt = nnz + n + 8;
+        uint64_t *tp = (uint64_t *)mem.alloc((nt + 1) * sizeof(uint64_t));
+        if (!tp) {
+            set_error("device allocation for the tag prefix failed");
+            return TC_E_OOM;
+        }
+        g->tagpre = tp;
+        g->tagpre_n = nt + 1;
+        if ((st = scan_exclusive<uint64_t>(mem, nt, TagIn{adj}, ArrayOutExcl<uint64_t>{tp},
+                                           tp + nt, s, &g->launches)) != TC_OK)
+            return st;
+        TC_CUDA(cudaStreamSynchronize(s));
+    }
     g->st.m_in = m;
     g->st.loops_dropped = loops;
     g->st.dyads = D;

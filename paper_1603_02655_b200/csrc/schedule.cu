@@ -48,7 +48,22 @@ __device__ __forceinline__ uint32_t digit_of(uint32_t c) {
 // merge trips (sum of t)
 struct PlanIn {
     const uint32_t *du, *de, *dc, *dt, *dpb, *ups, *off;
+    int sparse;   // skewed-pair items allowed (tag prefix built, 16-class mode)
 };
+
+// skewed-pair decision for a big dyad: 0 = merge items; 1 = iterate A (the
+// entries > u of N(u)) and search N(v); 2 = iterate B and search N(u).
+// *len = length of the iterated list.
+__device__ __forceinline__ uint32_t sparse_mode(const PlanIn &P, uint64_t i, uint32_t *len) {
+    const uint32_t u = __ldg(P.du + i), v = __ldg(P.de + i) >> 2;
+    const uint32_t a = __ldg(P.off + u + 1) - 1u - __ldg(P.ups + u);
+    const uint32_t b = __ldg(P.off + v + 1) - 1u - __ldg(P.dpb + i);
+    const uint32_t sh = a < b ? a : b, lg = a < b ? b : a;
+    const uint32_t lg2 = 32u - __clz(lg | 1u);
+    if ((uint64_t)sh * (lg2 + 4u) * 2u >= (uint64_t)a + b) return 0u;
+    *len = sh;
+    return a < b ? 1u : 2u;
+}
 
 __global__ void __launch_bounds__(kPlanThreads)
 k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
@@ -107,12 +122,13 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     // the tile's dyad arrays (L1/L2-resident) and stored coalesced at the end
     __shared__ uint16_t perm[kPlanTile];
     unsigned long long wt = 0, ww = 0, tt = 0, tw = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
+    unsigned long long nsp = 0, spc = 0;   // skewed-pair dyads and their sum of c
 #pragma unroll 4
     for (int k = 0; k < kPlanItems; k++) {
         const uint64_t i = tile0 + wbase + k * 32 + lane;
         const bool valid = i < N;
         const uint32_t c = cst[k], d = digit_of(c);
-        uint32_t nch = 0;
+        uint32_t nch = 0, smode = 0, span = 0;
         if (valid) {
             const uint32_t e = __ldg(P.de + i), pre = e & 3u;
             const uint32_t cf = __ldg(P.dc + i);
@@ -125,10 +141,16 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
                 wt += cf;
                 tt += c;
             } else {
-                nch = (c + kWarpChunk - 1) / kWarpChunk;
+                uint32_t slen = 0;
+                smode = (P.sparse && !mode64) ? sparse_mode(P, i, &slen) : 0u;
+                nch = smode ? max(1u, (slen + kSparseChunk - 1) / kSparseChunk)
+                            : (c + kWarpChunk - 1) / kWarpChunk;
                 ww += cf;
                 tw += c;
                 nbig++;
+                nsp += smode ? 1u : 0u;
+                spc += smode ? cf : 0u;
+                span = smode ? slen : c;
             }
         }
         // warp-aggregated cursor for the warp items
@@ -143,9 +165,10 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
             unsigned long long at = 0;
             if (lane == 31) at = atomicAdd(&stats[0], (unsigned long long)wtot);
             at = __shfl_sync(0xffffffffu, at, 31) + (incl - nch);
+            const uint32_t chunk = smode ? kSparseChunk : kWarpChunk;
             for (uint32_t q = 0; q < nch; q++) {
-                const uint32_t d0 = q * kWarpChunk;
-                wl[at + q] = BinItemW{(uint32_t)i, d0, min(c, d0 + kWarpChunk), 0u};
+                const uint32_t d0 = q * chunk;
+                wl[at + q] = BinItemW{(uint32_t)i, d0, min(span, d0 + chunk), smode};
             }
         }
     }
@@ -166,6 +189,8 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         dy1 += __shfl_xor_sync(0xffffffffu, dy1, o);
         dy2 += __shfl_xor_sync(0xffffffffu, dy2, o);
         dy3 += __shfl_xor_sync(0xffffffffu, dy3, o);
+        nsp += __shfl_xor_sync(0xffffffffu, nsp, o);
+        spc += __shfl_xor_sync(0xffffffffu, spc, o);
     }
     if (lane == 0) {
         if (wt) atomicAdd(&stats[1], wt);
@@ -173,6 +198,8 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         if (nbig) atomicAdd(&stats[3], nbig);
         if (tt) atomicAdd(&stats[4], tt);
         if (tw) atomicAdd(&stats[5], tw);
+        if (nsp) atomicAdd(&stats[8], nsp);
+        if (spc) atomicAdd(&stats[9], spc);
         if (mode64) {
             if (dy1) atomicAdd(&d_counts[1], dy1);
             if (dy2) atomicAdd(&d_counts[2], dy2);
@@ -332,10 +359,10 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
-    if ((st = stats.allocate(mem, 8)) != TC_OK) return st;
-    TC_CUDA(cudaMemsetAsync(stats.p, 0, 8 * sizeof(unsigned long long), s));
+    if ((st = stats.allocate(mem, 10)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(stats.p, 0, 10 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
-                   g->dyad_pb + k0, g->ups, g->off};
+                   g->dyad_pb + k0, g->ups, g->off, g->tagpre != nullptr};
     k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
         P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
         reinterpret_cast<unsigned long long *>(d_counts), mode64);
@@ -352,11 +379,12 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     lists.du = P.du;
     lists.de = P.de;
     lists.dpb = P.dpb;
+    lists.tagpre = g->tagpre;
     st = launch_bins(g, lists, s, d_counts, prof ? ev + 1 : nullptr, launches, mode64);
     if (st != TC_OK) return st;
     if (prof) {
         TC_CUDA(cudaEventRecord(ev[3], s));
-        unsigned long long hs[6];
+        unsigned long long hs[10];
         TC_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
         const uint64_t nt = N - hs[3];
@@ -373,7 +401,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->bin_items[0] = nt;
         prof->bin_items[1] = hs[0];
         prof->bin_items[2] = hs[3];   // dyads in the warp bin
-        prof->bin_items[3] = 0;
+        prof->bin_items[3] = hs[8];   // skewed-pair dyads (inside the warp bin)
         prof->bin_work[0] = hs[1];
         prof->bin_work[1] = hs[2];
         prof->bin_work[2] = hs[4];

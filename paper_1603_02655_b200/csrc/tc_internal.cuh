@@ -77,6 +77,13 @@ constexpr uint32_t kThreadBinMax = 254;    // c <= 254: one thread per dyad, sor
 constexpr uint32_t kLaneSpan = 255;        // max diagonals per lane (8-bit packed counters)
 constexpr uint32_t kWarpChunk = 32 * kLaneSpan;   // c > 254: warp items of <= 8160 diagonals
 constexpr int kNumBins = 2;
+// skewed-pair path (census.cu, schedule.cu): enabled on graphs with a row of
+// >= kSparseMinDegree entries; a big dyad whose short list s and long list l
+// satisfy s * (log2(l) + 4) * 2 < s + l is classified by binary searches of
+// the short list's entries in the long one (kSparseChunk short-list entries
+// per warp item) plus tag-count ranges of the long list
+constexpr uint64_t kSparseMinDegree = 4096;
+constexpr uint32_t kSparseChunk = 256;
 // per-dyad overhead of the shard cost model, in list-entry equivalents
 // (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
 constexpr uint64_t kShardKappa = 8;
@@ -104,6 +111,11 @@ struct tc_graph {
     uint32_t *dyad_pb = nullptr;
     uint32_t *dyad_t = nullptr;
     uint32_t *ups = nullptr;   size_t ups_n = 0;
+    // exclusive prefix over adj of (tag == 1) << 32 | (tag == 2), adj_n + 1
+    // entries; built only when some row is long (max degree >=
+    // kSparseMinDegree): the skewed-pair path of the warp bin counts the tags
+    // of a row range with two loads instead of a merge (census.cu)
+    uint64_t *tagpre = nullptr; size_t tagpre_n = 0;
     int profile = 0;
     tc_profile prof{};
     uint64_t launches = 0;

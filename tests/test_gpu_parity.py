@@ -297,3 +297,42 @@ def test_census64_vs_oracle(tcb):
         g = tcb.tc_graph_create(a.n, a.src, a.dst)
         assert tcb.tc_census64(g) == oracle.Graph(a.n, a.src, a.dst).census64(), a.meta
         g.close()
+
+
+def _hub_graph(seed):
+    """Two hubs (degree > kSparseMinDegree = 4096) inside a sparse random
+    digraph with mutual arcs and triangles: big dyads with one short and one
+    long list, so the warp bin takes the skewed-pair path (both modes)."""
+    rng = np.random.default_rng(seed)
+    n = 12000
+    leaves = rng.choice(np.arange(100, n), 7000, replace=False)
+    src = [np.full(7000, 5), leaves[:2000], rng.choice(np.arange(100, n), 6000), ]
+    dst = [leaves, np.full(2000, 5), np.full(6000, 17)]
+    src.append(rng.integers(0, n, 60000))          # background arcs
+    dst.append(rng.integers(0, n, 60000))
+    src.append(np.full(300, 17))                   # hub-hub and hub-leaf mutuals
+    dst.append(leaves[:300])
+    src.append(np.array([5, 17]))
+    dst.append(np.array([17, 5]))
+    s = np.concatenate(src).astype(np.uint32)
+    d = np.concatenate(dst).astype(np.uint32)
+    return n, s, d
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_skewed_pair_path_vs_oracle(tcb, seed):
+    n, s, d = _hub_graph(seed)
+    g = tcb.tc_graph_create(n, s, d)
+    try:
+        assert g.stats()["max_degree"] >= 4096
+        g.profile(True)
+        got = g.census()
+        prof = g.profile_get()
+        assert prof["bin_items"][3] > 0              # skewed-pair dyads were planned
+        og = oracle.Graph(n, s, d)
+        assert got == og.census()
+        D = g.stats()["dyads"]
+        for b, e in [(0, D // 3), (D // 3, D)]:
+            assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:]
+    finally:
+        g.close()
