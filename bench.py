@@ -348,7 +348,13 @@ def run_ours(args):
     bin_work = [profs[-1]["bin_work"][0], profs[-1]["bin_work"][1]]
     items = bin_dyads[dom]
     work = bin_work[dom]
-    bytes_alg = 4.0 * work + 24.0 * items      # 4(du+dv)+24 B per dyad
+    # 4(du+dv)+24 B per merged dyad; the warp bin's skewed-pair
+    # dyads (searched, not merged) count the entries they read instead
+    sp_dyads = int(profs[-1]["bin_items"][3]) if dom == 1 else 0
+    sp_c = int(profs[-1].get("sparse_sum_c", 0)) if dom == 1 else 0
+    sp_units = int(profs[-1].get("sparse_units", 0)) if dom == 1 else 0
+    bytes_merge_equiv = 4.0 * work + 24.0 * items
+    bytes_alg = 4.0 * (work - sp_c) + 24.0 * (items - sp_dyads) + 4.0 * sp_units + 24.0 * sp_dyads
     achieved = bytes_alg / (avg_k[dom] * 1e-3) / 1e9
     names = ["k_census_thread", "k_census_warp"]
     if args.mode == "64":
@@ -361,7 +367,8 @@ def run_ours(args):
     census_ms = float(np.mean([p["census_ms"] for p in profs]))
     plan_ms = float(np.mean([p["plan_ms"] for p in profs]))
     build_ms = float(np.mean([p["build_ms"] for p in profs]))
-    sum_all_bins_bytes = 4.0 * sum(bin_work) + 24.0 * sum(bin_dyads)
+    sp_all = (int(profs[-1].get("sparse_sum_c", 0)), int(profs[-1].get("sparse_units", 0)))
+    sum_all_bins_bytes = 4.0 * (sum(bin_work) - sp_all[0] + sp_all[1]) + 24.0 * sum(bin_dyads)
     m_arcs = a_m
     line = {"metric": METRIC, "value": m_arcs * args.steps / (total_ms * 1e-3), "unit": UNIT,
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -384,6 +391,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": names[dom],
                          "bytes_alg_per_launch": bytes_alg,
+                         "skewed_pair_dyads": sp_dyads,
+                         "merge_equivalent_frac": (bytes_merge_equiv / (avg_k[dom] * 1e-3) / 1e9) / hbm,
                          "peak_source": peak_src,
                          "all_bins_frac": (sum_all_bins_bytes / (sum(avg_k) * 1e-3) / 1e9) / hbm},
             "e2e": {"value": m_arcs * args.steps / (e2e_total * 1e-3), "unit": UNIT,

@@ -95,11 +95,15 @@ typedef struct {
     float plan_ms;          /* a2: per-dyad cost and degree bins */
     float census_ms;        /* a3+a4: all bin kernels incl. histogram flush */
     float kernel_ms[4];     /* a3+a4 per bin: [0] thread bin, [1] warp bin, [2..3] 0 */
-    uint64_t bin_items[4];  /* [0] thread-bin dyads, [1] warp items, [2] warp-bin dyads */
+    uint64_t bin_items[4];  /* [0] thread-bin dyads, [1] warp items, [2] warp-bin dyads,
+                               [3] of those, skewed-pair dyads (searched, not merged) */
     uint64_t bin_work[4];   /* [0] / [1] thread / warp bin: sum of |N(u)|+|N(v)| (the
                                paper's uniform work unit, SURVEY 8(d) B_alg);
                                [2] / [3]: merge trips actually walked (entries
                                w > u of both rows, census.cu) */
+    uint64_t sparse_sum_c;  /* skewed-pair dyads: sum of |N(u)|+|N(v)| (part of bin_work[1]) */
+    uint64_t sparse_units;  /* skewed-pair dyads: entries they read = sum over dyads of
+                               s * (ceil(log2 l) + 1) + 4 (s, l: short and long list) */
 } tc_profile;
 
 /* Build the device graph from an arc list (a1).

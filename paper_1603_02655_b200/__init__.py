@@ -93,7 +93,8 @@ class Graph:
         check(lib.tc_profile_get(self._h, ctypes.byref(p)), "tc_profile_get")
         return {"build_ms": p.build_ms, "plan_ms": p.plan_ms, "census_ms": p.census_ms,
                 "kernel_ms": list(p.kernel_ms), "bin_items": [int(x) for x in p.bin_items],
-                "bin_work": [int(x) for x in p.bin_work]}
+                "bin_work": [int(x) for x in p.bin_work], "sparse_sum_c": int(p.sparse_sum_c),
+                "sparse_units": int(p.sparse_units)}
 
     def launches(self) -> int:
         return int(lib.tc_launch_count(self._h))

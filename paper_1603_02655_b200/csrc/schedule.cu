@@ -23,6 +23,14 @@
 #include "census.cuh"
 #include "scan.cuh"
 
+// search-vs-merge cost ratio NUM/DEN (measured)
+#ifndef TC_SP_NUM
+#define TC_SP_NUM 1u
+#endif
+#ifndef TC_SP_DEN
+#define TC_SP_DEN 1u
+#endif
+
 namespace tc {
 
 namespace {
@@ -54,14 +62,16 @@ struct PlanIn {
 // skewed-pair decision for a big dyad: 0 = merge items; 1 = iterate A (the
 // entries > u of N(u)) and search N(v); 2 = iterate B and search N(u).
 // *len = length of the iterated list.
-__device__ __forceinline__ uint32_t sparse_mode(const PlanIn &P, uint64_t i, uint32_t *len) {
+__device__ __forceinline__ uint32_t sparse_mode(const PlanIn &P, uint64_t i, uint32_t *len,
+                                                uint32_t *units) {
     const uint32_t u = __ldg(P.du + i), v = __ldg(P.de + i) >> 2;
     const uint32_t a = __ldg(P.off + u + 1) - 1u - __ldg(P.ups + u);
     const uint32_t b = __ldg(P.off + v + 1) - 1u - __ldg(P.dpb + i);
     const uint32_t sh = a < b ? a : b, lg = a < b ? b : a;
     const uint32_t lg2 = 32u - __clz(lg | 1u);
-    if ((uint64_t)sh * (lg2 + 4u) * 2u >= (uint64_t)a + b) return 0u;
+    if ((uint64_t)sh * (lg2 + 4u) * TC_SP_NUM >= ((uint64_t)a + b) * TC_SP_DEN) return 0u;
     *len = sh;
+    *units = sh * lg2 + 4u;   // per short entry: ~log2(l) probes + the entry; 4 prefix/row loads
     return a < b ? 1u : 2u;
 }
 
@@ -122,7 +132,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     // the tile's dyad arrays (L1/L2-resident) and stored coalesced at the end
     __shared__ uint16_t perm[kPlanTile];
     unsigned long long wt = 0, ww = 0, tt = 0, tw = 0, nbig = 0, dy1 = 0, dy2 = 0, dy3 = 0;
-    unsigned long long nsp = 0, spc = 0;   // skewed-pair dyads and their sum of c
+    unsigned long long nsp = 0, spc = 0, spu = 0;   // skewed-pair dyads, sum of c, units
 #pragma unroll 4
     for (int k = 0; k < kPlanItems; k++) {
         const uint64_t i = tile0 + wbase + k * 32 + lane;
@@ -141,8 +151,9 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
                 wt += cf;
                 tt += c;
             } else {
-                uint32_t slen = 0;
-                smode = (P.sparse && !mode64) ? sparse_mode(P, i, &slen) : 0u;
+                uint32_t slen = 0, sunits = 0;
+                smode = (P.sparse && !mode64) ? sparse_mode(P, i, &slen, &sunits) : 0u;
+                spu += smode ? sunits : 0u;
                 nch = smode ? max(1u, (slen + kSparseChunk - 1) / kSparseChunk)
                             : (c + kWarpChunk - 1) / kWarpChunk;
                 ww += cf;
@@ -191,6 +202,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         dy3 += __shfl_xor_sync(0xffffffffu, dy3, o);
         nsp += __shfl_xor_sync(0xffffffffu, nsp, o);
         spc += __shfl_xor_sync(0xffffffffu, spc, o);
+        spu += __shfl_xor_sync(0xffffffffu, spu, o);
     }
     if (lane == 0) {
         if (wt) atomicAdd(&stats[1], wt);
@@ -200,6 +212,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         if (tw) atomicAdd(&stats[5], tw);
         if (nsp) atomicAdd(&stats[8], nsp);
         if (spc) atomicAdd(&stats[9], spc);
+        if (spu) atomicAdd(&stats[10], spu);
         if (mode64) {
             if (dy1) atomicAdd(&d_counts[1], dy1);
             if (dy2) atomicAdd(&d_counts[2], dy2);
@@ -359,8 +372,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
     if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
-    if ((st = stats.allocate(mem, 10)) != TC_OK) return st;
-    TC_CUDA(cudaMemsetAsync(stats.p, 0, 10 * sizeof(unsigned long long), s));
+    if ((st = stats.allocate(mem, 11)) != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(stats.p, 0, 11 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off, g->tagpre != nullptr};
     k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
@@ -384,7 +397,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     if (st != TC_OK) return st;
     if (prof) {
         TC_CUDA(cudaEventRecord(ev[3], s));
-        unsigned long long hs[10];
+        unsigned long long hs[11];
         TC_CUDA(cudaMemcpyAsync(hs, stats.p, sizeof(hs), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
         const uint64_t nt = N - hs[3];
@@ -406,6 +419,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->bin_work[1] = hs[2];
         prof->bin_work[2] = hs[4];
         prof->bin_work[3] = hs[5];
+        prof->sparse_sum_c = hs[9];
+        prof->sparse_units = hs[10];
         for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
     }
     return TC_OK;
