@@ -75,6 +75,7 @@ __device__ __forceinline__ uint32_t sparse_mode(const PlanIn &P, uint64_t i, uin
     return a < b ? 1u : 2u;
 }
 
+template <bool SPARSE>
 __global__ void __launch_bounds__(kPlanThreads)
 k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
             uint32_t *__restrict__ tile_count, BinItemW *__restrict__ wl,
@@ -152,7 +153,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
                 tt += c;
             } else {
                 uint32_t slen = 0, sunits = 0;
-                smode = (P.sparse && !mode64) ? sparse_mode(P, i, &slen, &sunits) : 0u;
+                smode = (SPARSE && P.sparse && !mode64) ? sparse_mode(P, i, &slen, &sunits) : 0u;
                 spu += smode ? sunits : 0u;
                 nch = smode ? max(1u, (slen + kSparseChunk - 1) / kSparseChunk)
                             : (c + kWarpChunk - 1) / kWarpChunk;
@@ -376,7 +377,12 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     TC_CUDA(cudaMemsetAsync(stats.p, 0, 11 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off, g->tagpre != nullptr};
-    k_plan_tile<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
+    if (P.sparse && !mode64)
+        k_plan_tile<true><<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
+        P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
+        reinterpret_cast<unsigned long long *>(d_counts), mode64);
+    else
+        k_plan_tile<false><<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
         P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
         reinterpret_cast<unsigned long long *>(d_counts), mode64);
     TC_CUDA(cudaGetLastError());
