@@ -314,10 +314,12 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
             BinItemT e{0, 0, 0, 0};
             if (valid) {
                 e = it[base + lane];
-                // the two parts are <= t entries each (their lengths are not
-                // in the item; the whole-diagonal merge needs no split)
-                prefetch_row_l2(adj, e.pa, e.t);
-                prefetch_row_l2(adj, e.pb, e.t);
+                // item word 3 = t | |A| << 16: prefetch exactly both parts
+                // (measured 0.856 vs 0.884 ms against t entries of each row)
+                const uint32_t alen = e.t >> 16;
+                e.t &= 0xffffu;
+                prefetch_row_l2(adj, e.pa, alen);
+                prefetch_row_l2(adj, e.pb, e.t - alen);
             }
             warp_reserve(c, wsh[warp], e.t);
             if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
@@ -594,7 +596,10 @@ k_census_thread64(const BinItemT *__restrict__ items, const uint32_t *__restrict
         for (uint32_t base = part + warp * 32; base < cnt; base += kCensusThreads) {
             const bool valid = base + lane < cnt;
             BinItemT e{0, 0, 0, 0};
-            if (valid) e = it[base + lane];
+            if (valid) {
+                e = it[base + lane];
+                e.t &= 0xffffu;
+            }
             warp_reserve64(S.hist[warp], S.tot[warp], c, e.t);
             if (valid)
                 merge_diag64(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, S.hist[warp], c);

@@ -189,7 +189,9 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) {
         const uint64_t i = tile0 + perm[j];
         const uint32_t u = __ldg(P.du + i);
-        out[j] = make_uint4(__ldg(P.ups + u), __ldg(P.dpb + i), __ldg(P.de + i), __ldg(P.dt + i));
+        // t | |A| << 16 (t <= 254): the census prefetches exactly both parts
+        const uint32_t pa = __ldg(P.ups + u), a = __ldg(P.off + u + 1) - 1u - pa;
+        out[j] = make_uint4(pa, __ldg(P.dpb + i), __ldg(P.de + i), __ldg(P.dt + i) | a << 16);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {

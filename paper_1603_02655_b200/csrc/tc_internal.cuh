@@ -88,8 +88,8 @@ constexpr uint32_t kSparseChunk = 256;
 // (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
 constexpr uint64_t kShardKappa = 8;
 
-struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, merge length t
-    uint32_t pa, pb, e, t;
+struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, t = merge length
+    uint32_t pa, pb, e, t;   // | (length of the A part) << 16 (both <= 254)
 };
 struct BinItemW {   // warp bin: dyad index (in the planned range), diagonals [d0, d1)
     uint32_t k, d0, d1, pad;
