@@ -38,7 +38,10 @@
  *    tc_census_range and tc_census_multi return after the stream has drained
  *    (results on the host); tc_census_enqueue does not synchronise.
  *  - A tc_graph may be shared read-only by concurrent census calls on
- *    different streams.
+ *    different streams (and host threads): a call keeps its launch count
+ *    and profile in its own locals and publishes them to the graph's
+ *    "most recent call" slot under a mutex at its end (tc_launch_count,
+ *    tc_profile_get report whichever call finished last).
  */
 #ifndef TRIADCENSUS_H
 #define TRIADCENSUS_H
@@ -103,7 +106,7 @@ typedef struct {
                                w > u of both rows, census.cu) */
     uint64_t sparse_sum_c;  /* skewed-pair dyads: sum of |N(u)|+|N(v)| (part of bin_work[1]) */
     uint64_t sparse_units;  /* skewed-pair dyads: entries they read = sum over dyads of
-                               s * (ceil(log2 l) + 1) + 4 (s, l: short and long list) */
+                               s * ceil(log2(l + 1)) + 4 (s, l: short and long list) */
 } tc_profile;
 
 /* Build the device graph from an arc list (a1).
@@ -152,21 +155,29 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
                       uint64_t *c0_hi);
 
 /* Partial census over canonical dyads [dyad_begin, dyad_end) (clamped to
- * [0, D)): classes 2..16 only, partial[0] = 0.  Partials over any partition
- * of [0, D) sum to the full census minus 003.  Classes 4..16
- * (021D..300) are exactly those of the range's canonical triads.
- * Classes 2..3 (012, 102): each dyad (u,v) of the range contributes
- * n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}| to its class, plus one
- * to the class of dyad (v,x) for every x > v in N(u) & N(v) -- the
- * intersection element u of that later dyad, which its own merge (starting
- * at entries > v) does not see (reading 21).  Synchronous. */
+ * [0, D)): classes 2..16 only, partial[0] = 0 -- exactly the loop of Fig.
+ * P:269-309 (lines 5-21) restricted to the dyads of the range in the
+ * algorithm's own order: each dyad (u,v) of the range adds its
+ * n - |S| - 2 dyadic triads to class 102 (mutual) or 012, and
+ * its canonical connected triads to their classes.  Every entry is
+ * a non-negative count; partials over any partition of [0, D) sum to the
+ * full census minus 003.  This is the test / shard hook: the full
+ * and multi-GPU census do not call it (they split 012 / 102 differently,
+ * see tc_census_enqueue).  Synchronous. */
 tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                           void *cuda_stream, uint64_t partial[16]);
 
 /* Asynchronous partial census: enqueues a2..a4 for dyads [dyad_begin,
  * dyad_end) on the stream and ADDS classes 2..16 into the device array
  * d_counts[16] (uint64, caller-owned, caller zeroes it).  No host sync and
- * no closing (unless profiling is on): bin sizes stay on the device. */
+ * no closing (unless profiling is on): bin sizes stay on the device.
+ * Classes 4..16 (021D..300) are exactly the range's (as tc_census_range).
+ * Classes 2..3 use the kernels' owed-credit attribution (DESIGN.md reading
+ * 21): dyad (u,v) adds n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}|
+ * to its class, plus one to the class of dyad (v,x) for every x > v in
+ * N(u) & N(v).  Summed over a partition of [0, D) this is the paper's total
+ * exactly; a single range's 012 / 102 may differ from tc_census_range and
+ * its uint64 slots are exact only modulo 2^64 (they can be "negative"). */
 tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                             void *cuda_stream, uint64_t *d_counts);
 
@@ -174,18 +185,23 @@ tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dya
  * 128-bit.  Returns TC_E_INVALID if the sum exceeds C(n,3). */
 tc_status tc_close_census(uint64_t n, uint64_t counts[16], uint64_t *c003_hi);
 
-/* Degree-balanced shard cuts: splits canonical
- * dyads [0, D) into `world` contiguous ranges of near-equal uniform cost
- * sum(|N(u)| + |N(v)| + kappa) (the paper's uniform workload, P:1693,
- * P:1837, applied across GPUs).  bounds[r], bounds[r+1] delimit rank r;
- * bounds must hold world+1 entries.  Host-only pure function over host
- * `cost` (per-dyad |N(u)|+|N(v)|, length D); the device path applies the
- * same rule to its device cost prefix. */
+/* Shard cuts: splits canonical dyads [0, D) into
+ * `world` contiguous ranges of near-equal sum(cost[k] + kappa): the paper's
+ * task-queue cut applied across GPUs.  bounds[r],
+ * bounds[r+1] delimit rank r; bounds must hold world+1 entries (1 <= world
+ * <= 1024).  bounds[r] = first k whose exclusive prefix of cost + kappa is
+ * >= floor(T r / world), T = the total.  Host-only pure function over host
+ * `cost` (length D). */
 tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint64_t kappa,
                                uint64_t *bounds);
 
-/* Same cut rule on the device graph (bounds for every rank, host array of
- * world+1 entries). */
+/* The cut the multi-GPU census uses, on the device graph (host array of
+ * world+1 entries): the same rule with kappa = 8 and cost[k] = the census
+ * kernels' own work for dyad k = (u,v) -- t = |{w in N(u): w > u}| +
+ * |{w in N(v): w > u}| merge trips, or, for a skewed-pair dyad (hub graphs,
+ * census.cu: short list s, long list l, s (ceil(log2(l + 1)) + 4) < s + l),
+ * s * ceil(log2(l + 1)) + 4 search units.  Computed once per world size and
+ * cached in the graph.  Errors: TC_E_INVALID (world outside [1, 1024]). */
 tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds);
 
 /* The multithreaded version's task queues, as a GPU scheduler (SURVEY.md
@@ -229,7 +245,8 @@ tc_status tc_comm_wrap(void *borrowed_nccl_comm, tc_comm **out);
 void tc_comm_destroy(tc_comm *c);
 
 /* Multi-GPU census: each rank holds the full graph (replicated CSR),
- * computes its degree-balanced shard of canonical dyads, and the 16 partial
+ * computes its work-balanced shard of canonical dyads (tc_shard_bounds: the
+ * cut is computed once per world size and cached), and the 16 partial
  * counts are summed by one ncclAllReduce (uint64, sum) on the stream.  Every
  * rank receives the identical full census (closing done after the
  * reduction).  Synchronous. */

@@ -6,6 +6,14 @@ independently of bm_oracle.c so the two can pin each other.
 * ``census_bm``    Fig. "Subquadratic Triad Census Algorithm" (P:269-309),
                    6-probe TriadCode, Python sets for N and S.
 * ``census_brute`` the naive O(n^3) census.
+* ``census_range_brute``  the per-dyad-range census by brute force over
+                   triples: a triple with exactly one connected pair is a
+                   dyadic triad of that pair (lines 9-14); a
+                   connected triple a < b < c belongs to its
+                   lexicographically smallest adjacent pair -- (a,b) if
+                   a~b, else (a,c) -- which is the one canonical dyad whose
+                   predicate (line 16: v < w, or u < w < v with w not
+                   adjacent to u) admits the third vertex.
 * ``man_digits``   the M, A, N digit counts of a code.
 The code->class map is taken as an argument (the table under test).
 """
@@ -50,6 +58,30 @@ def census_brute(n, src, dst, table):
     C = [0] * 17
     for a, b, c in combinations(range(n), 3):
         C[table[_code(E, a, b, c)]] += 1
+    return C[1:]
+
+
+def canonical_dyads(n, src, dst):
+    """Connected pairs (u, v), u < v, in the algorithm's order (u asc, v asc,
+    P:277-281)."""
+    return sorted({(min(int(a), int(b)), max(int(a), int(b)))
+                   for a, b in zip(src, dst) if int(a) != int(b)})
+
+
+def census_range_brute(n, src, dst, table, b, e):
+    """Classes 2..16 (element 0 = 0) of canonical dyads with index in [b, e)."""
+    E = _arcs(n, src, dst)
+    index = {d: k for k, d in enumerate(canonical_dyads(n, src, dst))}
+    adj = lambda x, y: (x, y) in E or (y, x) in E
+    C = [0] * 17
+    for a, bb, c in combinations(range(n), 3):
+        pairs = [p for p in ((a, bb), (a, c), (bb, c)) if adj(*p)]
+        if not pairs:
+            continue
+        k = index[pairs[0]]            # lexicographically smallest adjacent pair
+        if b <= k < e:
+            C[table[_code(E, a, bb, c)]] += 1
+    C[1] = 0
     return C[1:]
 
 

@@ -8,6 +8,7 @@
 #include <string.h>
 
 #include <string>
+#include <vector>
 
 #include "census.cuh"
 
@@ -216,11 +217,35 @@ tc_status tc_profile_get(const tc_graph *g, tc_profile *out) {
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
     return TC_OK;
 }
 
-uint64_t tc_launch_count(const tc_graph *g) { return g ? g->launches : 0; }
+uint64_t tc_launch_count(const tc_graph *g) {
+    if (!g) return 0;
+    std::lock_guard<std::mutex> lk(g->mu);
+    return g->launches;
+}
+
+// A census call counts its launches and records its profile in locals and
+// publishes them to the graph's "most recent call" slot once, under the
+// graph's mutex: concurrent census calls on a shared graph do not race.
+struct CallRec {
+    uint64_t launches = 0;
+    tc_profile prof{};
+    tc_profile *profp(const tc_graph *g) { return g->profile ? &prof : nullptr; }
+};
+
+static void publish(const tc_graph *g, const CallRec &r) {
+    std::lock_guard<std::mutex> lk(g->mu);
+    g->launches = r.launches;
+    if (g->profile) {
+        const float build = g->prof.build_ms;
+        g->prof = r.prof;
+        g->prof.build_ms = build;
+    }
+}
 
 tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_end,
                             void *cuda_stream, uint64_t *d_counts) {
@@ -229,15 +254,18 @@ tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dya
         return TC_E_INVALID;
     }
     TC_CUDA(cudaSetDevice(g->device));
-    tc_graph *mg = const_cast<tc_graph *>(g);
-    mg->launches = 0;
-    tc_profile *prof = g->profile ? &mg->prof : nullptr;
-    return census_range_device(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, d_counts, prof,
-                               &mg->launches);
+    CallRec r;
+    const tc_status st = census_range_device(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream,
+                                             d_counts, r.profp(g), &r.launches);
+    publish(g, r);
+    return st;
 }
 
+// paper = 1: classes 012 / 102 in the paper's per-dyad attribution (the
+// tc_census_range contract); 0: the owed-credit attribution of the full and
+// multi-GPU paths (reading 21; partials sum to the same census)
 static tc_status census_partial_sync(const tc_graph *g, uint64_t k0, uint64_t k1,
-                                     cudaStream_t s, uint64_t out[16]) {
+                                     cudaStream_t s, uint64_t out[16], int paper) {
     TC_CUDA(cudaSetDevice(g->device));
     Mem mem = g->mem;
     mem.stream = s;
@@ -245,7 +273,11 @@ static tc_status census_partial_sync(const tc_graph *g, uint64_t k0, uint64_t k1
     tc_status st = d.allocate(mem, 16);
     if (st != TC_OK) return st;
     TC_CUDA(cudaMemsetAsync(d.p, 0, 16 * sizeof(uint64_t), s));
-    if ((st = tc_census_enqueue(g, k0, k1, s, d.p)) != TC_OK) return st;
+    CallRec r;
+    st = paper ? census_range_paper_device(g, k0, k1, s, d.p, r.profp(g), &r.launches)
+               : census_range_device(g, k0, k1, s, d.p, r.profp(g), &r.launches);
+    publish(g, r);
+    if (st != TC_OK) return st;
     TC_CUDA(cudaMemcpyAsync(out, d.p, 16 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
     out[0] = 0;
@@ -257,7 +289,7 @@ tc_status tc_census(const tc_graph *g, void *cuda_stream, uint64_t counts[16], u
         set_error("NULL argument");
         return TC_E_INVALID;
     }
-    tc_status st = census_partial_sync(g, 0, g->st.dyads, (cudaStream_t)cuda_stream, counts);
+    tc_status st = census_partial_sync(g, 0, g->st.dyads, (cudaStream_t)cuda_stream, counts, 0);
     if (st != TC_OK) return st;
     return tc_close_census(g->st.n, counts, c003_hi);
 }
@@ -268,7 +300,7 @@ tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_
         set_error("NULL argument");
         return TC_E_INVALID;
     }
-    return census_partial_sync(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, partial);
+    return census_partial_sync(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, partial, 1);
 }
 
 tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
@@ -285,10 +317,9 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
     tc_status st = d.allocate(mem, 64);
     if (st != TC_OK) return st;
     TC_CUDA(cudaMemsetAsync(d.p, 0, 64 * sizeof(uint64_t), s));
-    tc_graph *mg = const_cast<tc_graph *>(g);
-    mg->launches = 0;
-    st = census_range_device(g, 0, g->st.dyads, s, d.p, g->profile ? &mg->prof : nullptr,
-                             &mg->launches, 1);
+    CallRec r;
+    st = census_range_device(g, 0, g->st.dyads, s, d.p, r.profp(g), &r.launches, 1);
+    publish(g, r);
     if (st != TC_OK) return st;
     TC_CUDA(cudaMemcpyAsync(counts, d.p, 64 * sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
@@ -312,7 +343,7 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
 
 tc_status tc_shard_bounds_host(const uint64_t *cost, uint64_t D, int world, uint64_t kappa,
                                uint64_t *bounds) {
-    if (!bounds || world < 1 || world > 1024 || (D && !cost)) {
+    if (!bounds || world < 1 || world > kMaxWorld || (D && !cost)) {
         set_error("invalid shard arguments");
         return TC_E_INVALID;
     }
@@ -349,7 +380,7 @@ tc_status tc_task_queues(const tc_graph *g, int strategy, uint64_t max_nset_size
 }
 
 tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint64_t *bounds) {
-    if (!g || !bounds || world < 1 || world > 1024) {
+    if (!g || !bounds || world < 1 || world > kMaxWorld) {
         set_error("invalid shard arguments");
         return TC_E_INVALID;
     }
@@ -442,7 +473,7 @@ tc_status tc_comm_unique_id(uint8_t id[128]) {
 }
 
 tc_status tc_comm_create(const uint8_t id[128], int world, int rank, int device, tc_comm **out) {
-    if (!id || !out || world < 1 || rank < 0 || rank >= world) {
+    if (!id || !out || world < 1 || world > kMaxWorld || rank < 0 || rank >= world) {
         set_error("invalid communicator arguments");
         return TC_E_INVALID;
     }
@@ -482,6 +513,10 @@ tc_status tc_comm_wrap(void *borrowed_nccl_comm, tc_comm **out) {
     if ((rc = n->count(cm, &world))) return nccl_fail(n, rc, "ncclCommCount");
     if ((rc = n->user_rank(cm, &rank))) return nccl_fail(n, rc, "ncclCommUserRank");
     if ((rc = n->cu_device(cm, &dev))) return nccl_fail(n, rc, "ncclCommCuDevice");
+    if (world < 1 || world > kMaxWorld) {
+        set_error("communicator of %d ranks: at most %d supported", world, kMaxWorld);
+        return TC_E_INVALID;
+    }
     tc_comm *c = new tc_comm();
     c->comm = cm;
     c->world = world;
@@ -512,8 +547,8 @@ tc_status tc_census_multi(const tc_graph *g, tc_comm *comm, void *cuda_stream,
     }
     TC_CUDA(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)cuda_stream;
-    uint64_t bounds[1025];
-    tc_status st = shard_bounds_device(g, comm->world, s, kShardKappa, bounds);
+    std::vector<uint64_t> bounds((size_t)comm->world + 1);
+    tc_status st = shard_bounds_device(g, comm->world, s, kShardKappa, bounds.data());
     if (st != TC_OK) return st;
     Mem mem = g->mem;
     mem.stream = s;

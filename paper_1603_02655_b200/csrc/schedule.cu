@@ -20,6 +20,8 @@
 // queues with one "queue" per GPU.
 #include <stdlib.h>
 
+#include <vector>
+
 #include "census.cuh"
 #include "scan.cuh"
 
@@ -226,11 +228,22 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     }
 }
 
-struct CostIn {
-    const uint32_t *dc;
+// Shard cost of canonical dyad k (refined to the
+// work the census kernels actually do): kappa + t for a merged dyad (t merge
+// trips over the entries w > u of both rows, census.cu), kappa + the search
+// units s * ceil(log2 l) + 4 for a skewed-pair dyad (same rule as the plan).
+// The paper's uniform estimate |N(u)| + |N(v)| - 2 weighs
+// early dyads (small u) too lightly: their merges walk more of both rows.
+struct WorkIn {
+    PlanIn P;
     uint64_t kappa;
     __device__ __forceinline__ uint64_t operator()(size_t k) const {
-        return (uint64_t)__ldg(dc + k) + kappa;
+        const uint32_t t = __ldg(P.dt + k);
+        if (P.sparse && t > kThreadBinMax) {
+            uint32_t len = 0, units = 0;
+            if (sparse_mode(P, k, &len, &units)) return (uint64_t)units + kappa;
+        }
+        return (uint64_t)t + kappa;
     }
 };
 
@@ -343,7 +356,88 @@ __global__ void __launch_bounds__(32) k_queue_greedy(const uint32_t *__restrict_
         out[1] = total;
     }
 }
+// tc_census_range's per-range dyadic triads in the paper's own attribution
+// (Fig. P:269-309 lines 9-14): every canonical dyad (u, v) of the range adds
+// n - |S| - 2 = n - |N(u)| - |N(v)| + |N(u) & N(v)| (S = N(u) U N(v) \ {u,v};
+// u, v are not in the intersection: no loops) to class 102 if pre = 3, else
+// 012.  One warp per dyad: lanes take the entries of the shorter row and
+// binary-search them in the longer one (rows are sorted by id).  Classes
+// 021D..300 of the range are exact per range in the bin kernels' partial
+// `part`, which block 0 adds (its 012 / 102 slots use the owed-credit
+// attribution of DESIGN.md reading 21 and are dropped here).
+__global__ void __launch_bounds__(256)
+k_range_dyadic(const uint32_t *__restrict__ off, const uint32_t *__restrict__ adj,
+               const uint32_t *__restrict__ du, const uint32_t *__restrict__ de, uint64_t N,
+               uint64_t n, const unsigned long long *__restrict__ part,
+               unsigned long long *__restrict__ d_counts) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    unsigned long long a012 = 0, a102 = 0;
+    for (uint64_t k = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; k < N; k += nw) {
+        const uint32_t u = __ldg(du + k), e = __ldg(de + k), v = e >> 2;
+        uint32_t oa = __ldg(off + u), la = __ldg(off + u + 1) - 1u - oa;
+        uint32_t ob = __ldg(off + v), lb = __ldg(off + v + 1) - 1u - ob;
+        const uint32_t dsum = la + lb;
+        if (la > lb) {
+            uint32_t t = oa; oa = ob; ob = t;
+            t = la; la = lb; lb = t;
+        }
+        uint32_t hits = 0;
+        for (uint32_t i = lane; i < la; i += 32) {
+            const uint32_t x = __ldg(adj + oa + i) >> 2;
+            uint32_t lo = 0, hi = lb;
+            while (lo < hi) {
+                const uint32_t mid = (lo + hi) >> 1;
+                if ((__ldg(adj + ob + mid) >> 2) < x) lo = mid + 1;
+                else hi = mid;
+            }
+            hits += (lo < lb && (__ldg(adj + ob + lo) >> 2) == x);
+        }
+        hits = __reduce_add_sync(0xffffffffu, hits);
+        const unsigned long long dy = n - dsum + hits;
+        if ((e & 3u) == 3u) a102 += lane == 0 ? dy : 0ull;
+        else a012 += lane == 0 ? dy : 0ull;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        a012 += __shfl_xor_sync(0xffffffffu, a012, o);
+        a102 += __shfl_xor_sync(0xffffffffu, a102, o);
+    }
+    if (lane == 0) {
+        if (a012) atomicAdd(&d_counts[1], a012);
+        if (a102) atomicAdd(&d_counts[2], a102);
+    }
+    if (blockIdx.x == 0 && threadIdx.x >= 3 && threadIdx.x < 16 && part[threadIdx.x])
+        atomicAdd(&d_counts[threadIdx.x], part[threadIdx.x]);
+}
+
 }  // namespace
+
+tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
+                                    uint64_t *d_counts, tc_profile *prof, uint64_t *launches) {
+    const uint64_t D = g->st.dyads;
+    if (k1 > D) k1 = D;
+    if (k0 >= k1) return TC_OK;
+    Mem mem = g->mem;
+    mem.stream = s;
+    DevBuf<uint64_t> part;
+    tc_status st = part.allocate(mem, 16);
+    if (st != TC_OK) return st;
+    TC_CUDA(cudaMemsetAsync(part.p, 0, 16 * sizeof(uint64_t), s));
+    if ((st = census_range_device(g, k0, k1, s, part.p, prof, launches)) != TC_OK) return st;
+    const uint64_t N = k1 - k0;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    uint64_t blocks = (N + 7) / 8;
+    if (blocks > (uint64_t)sms * 8) blocks = (uint64_t)sms * 8;
+    k_range_dyadic<<<(unsigned)blocks, 256, 0, s>>>(
+        g->off, g->adj, g->dyad_u + k0, g->dyad_e + k0, N, g->st.n,
+        reinterpret_cast<const unsigned long long *>(part.p),
+        reinterpret_cast<unsigned long long *>(d_counts));
+    TC_CUDA(cudaGetLastError());
+    *launches += 1;
+    return TC_OK;
+}
 
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
                               uint64_t *d_counts, tc_profile *prof, uint64_t *launches,
@@ -485,38 +579,54 @@ tc_status task_queues_device(const tc_graph *g, int nonuniform, uint64_t max_nse
 
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
                               uint64_t *bounds) {
-    const uint64_t D = g->st.dyads;
-    bounds[0] = 0;
-    bounds[world] = D;
-    if (world == 1) return TC_OK;
-    if (world > 1024) {
-        set_error("world %d > 1024", world);
+    if (world < 1 || world > kMaxWorld) {
+        set_error("world %d outside [1, %d]", world, kMaxWorld);
         return TC_E_INVALID;
     }
-    Mem mem = g->mem;
-    mem.stream = s;
-    tc_status st;
-    DevBuf<uint64_t> excl, tot, tg, out;
-    if ((st = excl.allocate(mem, D)) != TC_OK) return st;
-    if ((st = tot.allocate(mem, 1)) != TC_OK) return st;
-    st = scan_exclusive<uint64_t>(mem, D, CostIn{g->dyad_c, kappa}, ArrayOutExcl<uint64_t>{excl.p},
-                                  tot.p, s, nullptr);
-    if (st != TC_OK) return st;
-    uint64_t T = 0;
-    TC_CUDA(cudaMemcpyAsync(&T, tot.p, sizeof(T), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    uint64_t targets[1024];
-    for (int r = 1; r < world; r++)
-        targets[r - 1] = (uint64_t)(((unsigned __int128)T * (unsigned)r) / (unsigned)world);
-    if ((st = tg.allocate(mem, world)) != TC_OK) return st;
-    if ((st = out.allocate(mem, world)) != TC_OK) return st;
-    TC_CUDA(cudaMemcpyAsync(tg.p, targets, (world - 1) * sizeof(uint64_t), cudaMemcpyHostToDevice,
-                            s));
-    k_lower_bounds<<<1, 1024, 0, s>>>(excl.p, D, tg.p, world - 1, out.p);
-    TC_CUDA(cudaGetLastError());
-    TC_CUDA(cudaMemcpyAsync(bounds + 1, out.p, (world - 1) * sizeof(uint64_t),
-                            cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
+    const uint64_t D = g->st.dyads;
+    {   // cached per world size (the graph is immutable after the build)
+        std::lock_guard<std::mutex> lk(g->mu);
+        auto it = g->shard_cache.find(world);
+        if (it != g->shard_cache.end() && kappa == kShardKappa) {
+            for (int r = 0; r <= world; r++) bounds[r] = it->second[r];
+            return TC_OK;
+        }
+    }
+    bounds[0] = 0;
+    bounds[world] = D;
+    if (world > 1 && D > 0) {
+        Mem mem = g->mem;
+        mem.stream = s;
+        tc_status st;
+        DevBuf<uint64_t> excl, tot, tg, out;
+        if ((st = excl.allocate(mem, D)) != TC_OK) return st;
+        if ((st = tot.allocate(mem, 1)) != TC_OK) return st;
+        const PlanIn P{g->dyad_u, g->dyad_e, g->dyad_c, g->dyad_t, g->dyad_pb, g->ups, g->off,
+                       g->tagpre != nullptr};
+        st = scan_exclusive<uint64_t>(mem, D, WorkIn{P, kappa}, ArrayOutExcl<uint64_t>{excl.p},
+                                      tot.p, s, nullptr);
+        if (st != TC_OK) return st;
+        uint64_t T = 0;
+        TC_CUDA(cudaMemcpyAsync(&T, tot.p, sizeof(T), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        std::vector<uint64_t> targets(world - 1);
+        for (int r = 1; r < world; r++)
+            targets[r - 1] = (uint64_t)(((unsigned __int128)T * (unsigned)r) / (unsigned)world);
+        if ((st = tg.allocate(mem, world)) != TC_OK) return st;
+        if ((st = out.allocate(mem, world)) != TC_OK) return st;
+        TC_CUDA(cudaMemcpyAsync(tg.p, targets.data(), (world - 1) * sizeof(uint64_t),
+                                cudaMemcpyHostToDevice, s));
+        k_lower_bounds<<<(unsigned)((world + 255) / 256), 256, 0, s>>>(excl.p, D, tg.p, world - 1,
+                                                                      out.p);
+        TC_CUDA(cudaGetLastError());
+        TC_CUDA(cudaMemcpyAsync(bounds + 1, out.p, (world - 1) * sizeof(uint64_t),
+                                cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+    }
+    if (kappa == kShardKappa) {
+        std::lock_guard<std::mutex> lk(g->mu);
+        g->shard_cache[world].assign(bounds, bounds + world + 1);
+    }
     return TC_OK;
 }
 

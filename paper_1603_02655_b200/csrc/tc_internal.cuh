@@ -17,7 +17,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "triadcensus.h"
 
@@ -87,6 +90,7 @@ constexpr uint32_t kSparseChunk = 256;
 // per-dyad overhead of the shard cost model, in list-entry equivalents
 // (8 B item + 16 B offsets ~ 6 entries; SURVEY.md section 8(e) kappa ~ 8)
 constexpr uint64_t kShardKappa = 8;
+constexpr int kMaxWorld = 1024;   // ranks a shard cut supports
 
 struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, t = merge length
     uint32_t pa, pb, e, t;   // | (length of the A part) << 16 (both <= 254)
@@ -117,8 +121,15 @@ struct tc_graph {
     // of a row range with two loads instead of a merge (census.cu)
     uint64_t *tagpre = nullptr; size_t tagpre_n = 0;
     int profile = 0;
-    tc_profile prof{};
-    uint64_t launches = 0;
+    // results of the most recent build / census call: written once at the
+    // end of a call from that call's own locals, under `mu` (a graph may be
+    // shared read-only by concurrent census calls on different streams)
+    mutable std::mutex mu;
+    mutable tc_profile prof{};
+    mutable uint64_t launches = 0;
+    // shard cuts per world size (tc_shard_bounds / tc_census_multi), computed
+    // once on first use, under `mu`
+    mutable std::map<int, std::vector<uint64_t>> shard_cache;
 };
 
 namespace tc {
@@ -129,6 +140,10 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
 tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
                               uint64_t *d_counts, tc_profile *prof, uint64_t *launches,
                               int mode64 = 0);  // a2-a4
+// tc_census_range: the same range census, but classes 012 / 102 in the
+// paper's per-dyad attribution n - |S| - 2 (schedule.cu k_range_dyadic)
+tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
+                                    uint64_t *d_counts, tc_profile *prof, uint64_t *launches);
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
                               uint64_t *bounds);                      // schedule.cu
 tc_status task_queues_device(const tc_graph *g, int nonuniform, uint64_t max_nset, cudaStream_t s,

@@ -101,33 +101,9 @@ def test_full_config_vs_golden(tcb, golden_dir, name):
     assert st == rec["stats"]
 
 
-def attributed_range(n, src, dst, b, e):
-    """Classes 012 / 102 of canonical dyads [b, e) as the CUDA path attributes
-    them (reading 21), restated from sets, for small graphs: dyad
-    (u, v) owns n - |N(u)| - |N(v)| + |{x > u : x in N(u) & N(v)}|, plus one
-    dyadic triad of dyad (v, x) for every x > v in N(u) & N(v) (the
-    intersection element u < v of dyad (v, x), met by this merge).  The sum
-    over any partition of [0, D) is the paper's n - |S| - 2 total."""
-    arcs = {(int(s), int(d)) for s, d in zip(src, dst) if s != d}
-    nb = {}
-    for s, d in arcs:
-        nb.setdefault(s, set()).add(d)
-        nb.setdefault(d, set()).add(s)
-    mutual = lambda x, y: (x, y) in arcs and (y, x) in arcs
-    dyads = sorted({(min(s, d), max(s, d)) for s, d in arcs})
-    out = [0, 0]
-    for u, v in dyads[b:e]:
-        common = nb[u] & nb[v]
-        own = n - len(nb[u]) - len(nb[v]) + sum(1 for x in common if x > u)
-        out[1 if mutual(u, v) else 0] += own
-        for x in common:
-            if x > v:
-                out[1 if mutual(v, x) else 0] += 1
-    return out
-
-
-def test_dyad_range_attribution_small(tcb):
-    # every class of a dyad range, exact, on small random digraphs
+def test_dyad_range_small(tcb):
+    # T6: every class of a dyad range, exact, on small random digraphs,
+    # including every single-dyad range of the first graphs
     for seed in range(6):
         a = synth.random_digraph(60 + 20 * seed, 0.08 + 0.02 * seed, seed=100 + seed)
         og = oracle.Graph(a.n, a.src, a.dst)
@@ -138,20 +114,19 @@ def test_dyad_range_attribution_small(tcb):
         tot = [0] * 16
         for b, e in zip(bounds[:-1], bounds[1:]):
             part = tcb.tc_census_range(g, b, e)
-            want = og.census_range(b, e)
-            assert part[3:] == want[3:], (seed, b, e)
-            assert part[1:3] == attributed_range(a.n, a.src, a.dst, b, e), (seed, b, e)
-            assert part[0] == 0
+            assert part == og.census_range(b, e), (seed, b, e)
             tot = [x + y for x, y in zip(tot, part)]
         assert tcb.tc_close_census(a.n, tot) == og.census()
+        if seed < 2:
+            for k in range(D):
+                assert tcb.tc_census_range(g, k, k + 1) == og.census_range(k, k + 1), (seed, k)
         g.close()
 
 
 @pytest.mark.parametrize("name", ["C2", "C3"])
 def test_dyad_range_parity(tcb, name):
-    # T6: random canonical-dyad ranges: classes 021D..300 equal the oracle's
-    # partial exactly; 012 / 102 move between ranges (reading 21),
-    # so they are checked through a partition of [0, D) that sums to the census
+    # T6: random canonical-dyad ranges, all 16 entries equal the oracle's
+    # partial (Fig. P:269-309 restricted to the range)
     a = synth.make_config(name)
     og = oracle.Graph(a.n, a.src, a.dst)
     D = og.stats()["dyads"]
@@ -161,9 +136,11 @@ def test_dyad_range_parity(tcb, name):
     for _ in range(4):
         b = int(rng.integers(cuts[-1], D))
         e = min(D, b + int(rng.integers(1, 20_000)))
-        assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:], (b, e)
+        assert tcb.tc_census_range(g, b, e) == og.census_range(b, e), (b, e)
         cuts += [b, e]
-    assert tcb.tc_census_range(g, D - 3, D + 100)[3:] == og.census_range(D - 3, D)[3:]
+    for k in rng.integers(0, D, size=20).tolist():   # single dyads
+        assert tcb.tc_census_range(g, k, k + 1) == og.census_range(k, k + 1), k
+    assert tcb.tc_census_range(g, D - 3, D + 100) == og.census_range(D - 3, D)
     assert tcb.tc_census_range(g, 5, 5) == [0] * 16
     cuts = sorted(set(cuts + [D]))
     tot = [0] * 16
@@ -173,20 +150,31 @@ def test_dyad_range_parity(tcb, name):
     g.close()
 
 
-def test_partials_sum_and_shard_bounds(tcb):
-    a = synth.make_config("C2")
+@pytest.mark.parametrize("name", ["C2", "hub"])
+def test_partials_sum_and_shard_bounds(tcb, name):
+    # the device shard cut (cached per world) equals the host cut rule over
+    # the kernels' work restated in numpy (tests/shard_work.py); the rank
+    # partials sum to the full census
+    from shard_work import dyad_work
+    if name == "hub":
+        n, s, d = _hub_graph(3)
+        a = synth.Arcs(n, s, d)
+    else:
+        a = synth.make_config(name)
     g = tcb.tc_graph_create(a.n, a.src, a.dst)
     full = g.census()
-    og = oracle.Graph(a.n, a.src, a.dst)
-    cost = og.dyad_costs()
+    _, cost = dyad_work(a.n, a.src, a.dst)
     for world in (1, 2, 3, 8):
         b = tcb.tc_shard_bounds(g, world)
         assert b == tcb.tc_shard_bounds_host(cost, world, kappa=8)
+        assert tcb.tc_shard_bounds(g, world) == b          # cached
         tot = [0] * 16
         for r in range(world):
             part = tcb.tc_census_range(g, b[r], b[r + 1])
             tot = [x + y for x, y in zip(tot, part)]
         assert tcb.tc_close_census(a.n, tot) == full
+    with pytest.raises(tcb.TCError, match="TC_E_INVALID"):
+        tcb.tc_shard_bounds(g, 1025)
     g.close()
 
 
@@ -207,8 +195,9 @@ def test_device_arcs_equal_host_arcs(tcb):
     g.close()
 
 
-def test_closed_form_hub_star_block_bin_and_high_word(tcb):
-    # cost 2e5+1 per dyad -> block bin; n = 1e7 -> 003 needs the high word
+def test_closed_form_hub_star_warp_bin_and_high_word(tcb):
+    # cost 2e5+1 per dyad -> warp-bin items (skewed pairs); n = 1e7 -> 003
+    # needs the high word
     n, k = 10_000_000, 200_000
     for gen, cp, cs in ((synth.out_star, "012", "021D"), (synth.mutual_star, "102", "201")):
         a = gen(k, n)
@@ -236,7 +225,7 @@ def test_closed_form_tournament_clique_bipartite_cycle(tcb):
 
 
 def test_mixed_bins_skewed_rmat(tcb):
-    # R-MAT scale 12 edge factor 16: dyads in thread, warp and block bins
+    # R-MAT scale 12 edge factor 16: dyads in both the thread and warp bins
     a = synth.rmat(scale=12, edge_factor=16, seed=99)
     g = tcb.tc_graph_create(a.n, a.src, a.dst)
     g.profile(True)
@@ -333,6 +322,6 @@ def test_skewed_pair_path_vs_oracle(tcb, seed):
         assert got == og.census()
         D = g.stats()["dyads"]
         for b, e in [(0, D // 3), (D // 3, D)]:
-            assert tcb.tc_census_range(g, b, e)[3:] == og.census_range(b, e)[3:]
+            assert tcb.tc_census_range(g, b, e) == og.census_range(b, e)
     finally:
         g.close()

@@ -195,6 +195,27 @@ def test_dyad_range_partials_sum_to_full():
         assert oracle.choose3(n) - sum(tot) == full[0]
 
 
+def test_dyad_range_partials_vs_brute_force_attribution():
+    # og_census_range range by range (all 16 entries) against triples
+    # enumerated by brute force and attributed to their counting dyad
+    # (pyref.census_range_brute: the lexicographically smallest adjacent pair)
+    T = oracle.triad_table()
+    for s in range(24):
+        n = 6 + s % 11
+        a = synth.random_digraph(n, (0.15, 0.35, 0.7)[s % 3], seed=5000 + s, loops=True, dups=2)
+        g = oracle.Graph(n, a.src, a.dst)
+        D = g.stats()["dyads"]
+        assert len(pyref.canonical_dyads(n, a.src, a.dst)) == D
+        rng = np.random.default_rng(s)
+        cuts = sorted(set([0, D] + rng.integers(0, D + 1, size=4).tolist()))
+        for b, e in zip(cuts[:-1], cuts[1:]):
+            assert g.census_range(b, e) == pyref.census_range_brute(n, a.src, a.dst, T, b, e), \
+                (s, b, e)
+        for k in range(D):              # every single dyad
+            assert g.census_range(k, k + 1) == pyref.census_range_brute(n, a.src, a.dst, T, k,
+                                                                        k + 1), (s, k)
+
+
 def test_golden_files_are_complete(golden_dir):
     for name in ("C1", "C2", "C3"):
         p = os.path.join(golden_dir, "census_%s.json" % name)
