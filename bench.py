@@ -11,12 +11,17 @@ per second, timed with CUDA events on the launch stream, max over ranks.
 `e2e` = the same through the C ABI with HOST (pinned) arc buffers, the H2D
 copy and the result D2H inside the timed region.
 
-N > 1 (torchrun): every rank holds the replicated CSR, computes its
-degree-balanced dyad shard, and the 16 partial counts meet in one NCCL
-allreduce (tc_census_multi) -- strong scaling of one census.
+N > 1: `bench.py --gpus N` starts N ranks itself (torch.distributed.run on
+127.0.0.1) unless it already runs under a launcher (WORLD_SIZE set).  Every
+rank holds the replicated CSR, computes its work-balanced canonical-dyad
+shard, and the 16 partial counts meet in one NCCL allreduce
+(tc_census_multi) -- strong scaling of one census.
 
---impl reference: the CPU oracle (oracle/, plain single-threaded C) timed on
-the host on a bounded sample of the same workload; rank 0 only.
+--impl reference: the CPU oracle (oracle/, plain single-threaded C) on one
+pinned host core; its K steps are K equal-cost canonical-dyad ranges that
+cover the census once, so the line is one measured full census; rank 0 only.
+cpu_baseline (our arm, rank 0, N = 1): the same oracle over the whole census
+in forked single-threaded processes on the host's cores (bounded wall time).
 """
 from __future__ import annotations
 
@@ -52,8 +57,8 @@ def parse():
     p.add_argument("--mode", default="16", choices=["16", "64"],
                    help="16-class isomorphic census (default) or the 64-type census (f1)")
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--cpu-seconds", type=float, default=15.0,
-                   help="bounded oracle sample for cpu_baseline")
+    p.add_argument("--cpu-seconds", type=float, default=25.0,
+                   help="wall-time budget of the cpu_baseline oracle run (full census if it fits)")
     return p.parse_args()
 
 
@@ -132,52 +137,73 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU oracle baseline (rank 0, N = 1; and --impl reference)
 # ---------------------------------------------------------------------------
-def oracle_rate(a, seconds, steps=1):
-    """Time the oracle (as it stands) on a bounded sample: its graph build
-    (a1) once, then `steps` census samples, each a contiguous canonical-dyad
-    range sized to about `seconds`/steps of work, and extrapolate linearly
-    in the paper's uniform work units sum(|N(u)|+|N(v)|) to the whole census."""
+def host_cpu():
+    """lscpu model, logical CPUs, the affinity set."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True,
+                                   timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    aff = sorted(os.sched_getaffinity(0))
+    return {"model": model, "logical_cpus": os.cpu_count(), "affinity": len(aff),
+            "affinity_first": aff[0] if aff else None}
+
+
+def oracle_full_census(a, procs, budget_s=None):
+    """The oracle (as it stands) over the whole census: its graph build
+    (a1) once, then og_census_range over equal-cost canonical-dyad ranges in
+    `procs` forked single-threaded processes (oracle/sharded.py), summed and
+    closed.  If a calibration says one full pass would exceed `budget_s`
+    of wall time, only a systematic sample of the ranges (every j-th) runs
+    and the rate is extrapolated in the paper's uniform work units."""
     import oracle
+    from oracle import sharded
     t0 = time.perf_counter()
     g = oracle.Graph(a.n, a.src, a.dst)
     t_build = time.perf_counter() - t0
-    cost = g.dyad_costs().astype(np.float64)
-    total = float(cost.sum()) or 1.0
-    pre = np.concatenate([[0.0], np.cumsum(cost)])
-    # calibrate: time a tiny range first
-    per_unit = None
-    k = 0
-    probe = int(np.searchsorted(pre, total * 0.002))
-    t0 = time.perf_counter()
-    g.census_range(0, max(probe, 1))
-    dt = time.perf_counter() - t0
-    per_unit = dt / max(pre[max(probe, 1)], 1.0)
-    k = max(probe, 1)
-    step_times, step_units = [], []
-    for _ in range(steps):
-        want = seconds / steps / max(per_unit, 1e-12)
-        e = int(np.searchsorted(pre, pre[k] + want))
-        e = min(max(e, k + 1), cost.size)
-        if k >= cost.size:
-            k = 0
-            e = min(int(np.searchsorted(pre, want)), cost.size)
-        t0 = time.perf_counter()
-        g.census_range(k, e)
-        dt = time.perf_counter() - t0
-        step_times.append(dt)
-        step_units.append(pre[e] - pre[k])
-        per_unit = dt / max(pre[e] - pre[k], 1.0)
-        k = e
-    rate_units = sum(step_units) / sum(step_times)
-    t_census_full = total / rate_units
-    t_full = t_build + t_census_full
-    frac = sum(step_units) / total
-    return {"value": a.m / t_full, "t_full_s": t_full, "t_build_s": t_build,
-            "t_census_full_s": t_census_full, "sample_frac": frac,
-            "step_times": step_times, "step_units": step_units, "total_units": total}
+    cost = g.dyad_costs()
+    chunks = max(8 * procs, 64)
+    ranges = sharded.equal_cost_ranges(cost, chunks)
+    pre = np.concatenate([[0], np.cumsum(cost.astype(np.float64) + sharded.KAPPA)])
+    units = [pre[e] - pre[b] for b, e in ranges]
+    sample = list(range(len(ranges)))
+    if budget_s is not None:
+        # calibrate on one middle range, single process
+        mid = len(ranges) // 2
+        _, _, c1 = sharded.census_ranges(g, [ranges[mid]], 1)
+        est_wall = c1 * len(ranges) / max(procs, 1)
+        if est_wall > budget_s:
+            keep = max(procs, int(len(ranges) * budget_s / est_wall))
+            step = max(1, len(ranges) // keep)
+            sample = list(range(step // 2, len(ranges), step))
+    parts, wall, cpu = sharded.census_ranges(g, [ranges[i] for i in sample], procs)
+    full = len(sample) == len(ranges)
+    frac = sum(units[i] for i in sample) / pre[-1]
+    census = sharded.close(a.n, [parts[r] for r in ranges]) if full else None
+    t_census = wall / frac
+    return {"value": a.m / (t_build + t_census), "t_build_s": t_build, "t_census_s": t_census,
+            "wall_s": wall, "cpu_s": cpu, "procs": procs, "ranges": len(ranges),
+            "ranges_run": len(sample), "work_frac": frac, "full": full, "census": census}
+
+
+def golden_census(name):
+    p = os.path.join(ROOT, "tests", "golden", "census_%s.json" % name)
+    if os.path.exists(p):
+        return [int(x) for x in json.load(open(p))["census"]]
+    return None
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (oracle/, plain single-threaded C)
+    on one pinned host core.  The K timed steps are K contiguous equal-cost
+    canonical-dyad ranges that together cover [0, D), each one
+    og_census_range call: their sum is one MEASURED full census (after the
+    oracle's own graph build, timed once and charged to the steps), summed
+    and closed, and checked against tests/golden/ when present.  The W
+    warm-up steps re-run the first W ranges (untimed)."""
     rank, _, world = env_rank()
     if rank != 0:
         return 0
@@ -186,36 +212,63 @@ def run_reference(args):
                           "(synth/device.py); the CPU oracle runs on host-drawn configs only"
                           % args.config}), flush=True)
         return 0
+    import oracle
+    from oracle import sharded
+    cpu = host_cpu()
+    if cpu["affinity_first"] is not None:
+        os.sched_setaffinity(0, {cpu["affinity_first"]})     # one pinned core
     a = synth.make_config(args.config)
     steps = max(args.steps, 1)
-    per_step = max(2.0, min(8.0, 150.0 / (steps + args.warmup)))
-    r = oracle_rate(a, per_step * (steps + args.warmup), steps=steps + args.warmup)
-    times = r["step_times"][args.warmup:]
-    units = r["step_units"][args.warmup:]
-    rate_units = sum(units) / sum(times)
-    t_full = r["t_build_s"] + r["total_units"] / rate_units
-    value = a.m / t_full
-    sample = ("oracle build of the full graph once (%.1f s) + %d timed census samples of "
-              "contiguous canonical-dyad ranges (%.1f%% of sum(|N(u)|+|N(v)|) in total), "
-              "extrapolated linearly to the whole census" %
-              (r["t_build_s"], steps, 100 * sum(units) / r["total_units"]))
+    t0 = time.perf_counter()
+    g = oracle.Graph(a.n, a.src, a.dst)
+    t_build = time.perf_counter() - t0
+    st = g.stats()
+    ranges = sharded.equal_cost_ranges(g.dyad_costs(), steps)
+    for b, e in ranges[:args.warmup]:
+        g.census_range(b, e)
+    times, parts = [], []
+    for b, e in ranges:
+        t0 = time.perf_counter()
+        parts.append(g.census_range(b, e))
+        times.append(time.perf_counter() - t0)
+    census = sharded.close(a.n, parts)
+    gold = golden_census(args.config)
+    total = t_build + sum(times)
+    value = a.m / total
+    k = len(ranges)
+    sample = ("one full census measured: the oracle's graph build (%.2f s) + %d contiguous "
+              "equal-cost canonical-dyad ranges covering [0, D) (one og_census_range call per "
+              "step, %.2f s in total), single-threaded on one pinned core (%s)" %
+              (t_build, k, sum(times), cpu["model"]))
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
-            "n_gpus": world, "steps": steps, "warmup": args.warmup,
-            "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong",
+            "n_gpus": world, "steps": k, "warmup": args.warmup,
+            "ms_per_step": total * 1e3 / k, "higher_is_better": True,
+            "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config_of(a, None),
+            "config": bench_config(a, st, world),
+            "step_s": [round(x, 4) for x in times], "oracle_build_s": t_build,
+            "census_matches_golden": (census == gold) if gold else None,
+            "census": [str(x) for x in census],
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "host": cpu},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_of(a, stats, m_drawn=None):
+def bench_config(a, stats, world, m_drawn=None):
+    """The workload description both arms print unchanged (config)."""
+    m = a.m if m_drawn is None else m_drawn
     c = {"workload": "%s: %s" % (a.meta.get("config"), a.meta.get("label")),
          "generator": a.meta.get("generator"), "seed": a.meta.get("seed"), "n": a.n,
-         "m_drawn": a.m if m_drawn is None else m_drawn}
+         "m_drawn": m,
+         "l2": "%s (arcs %.0f MB, sort keys + scratch %.0f MB); the GPU arm writes a 512 MB "
+               "buffer (L2 flush) before every timed step"
+               % ("inputs > L2" if 8 * m > 126e6 else "inputs fit in L2", 8 * m / 1e6,
+                  16 * m / 1e6),
+         "parallelism": ("dp%d: replicated CSR, work-balanced canonical-dyad shards, one NCCL "
+                         "allreduce of 16 counts" % world) if world > 1 else "single GPU"}
     if stats:
         c.update({"m": stats["m"], "dyads": stats["dyads"], "sum_deg_sq": stats["sum_deg_sq"],
                   "max_degree": stats["max_degree"]})
@@ -228,8 +281,8 @@ def config_of(a, stats, m_drawn=None):
 def run_ours(args):
     import torch
     rank, local, world = env_rank()
-    if world != args.gpus and not (world == 1 and args.gpus == 1):
-        print("warning: --gpus %d but WORLD_SIZE %d" % (args.gpus, world), file=sys.stderr)
+    if world != args.gpus:
+        raise SystemExit("bench.py: --gpus %d but WORLD_SIZE %d" % (args.gpus, world))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -374,13 +427,9 @@ def run_ours(args):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": dict(config_of(a, stats, a_m), **{
-                "l2": "inputs > L2 (arcs %.0f MB, sort keys %.0f MB) and a 512 MB L2 flush "
-                      "before every timed step" % (8 * a_m / 1e6, 32 * a_m / 1e6),
-                "step": "a1 build from device arcs + a2 plan + a3/a4 kernels + a5 closing",
-                "census_mode": "64-type (f1)" if args.mode == "64" else "16-class",
-                "parallelism": "dp%d (replicated CSR, degree-balanced dyad shards, 1 NCCL "
-                               "allreduce)" % world if world > 1 else "single GPU"}),
+            "config": bench_config(a, stats, world, a_m),
+            "step": "a1 build from device arcs + a2 plan + a3/a4 kernels + a5 closing",
+            "census_mode": "64-type (f1)" if args.mode == "64" else "16-class",
             "phases_ms": {"build": build_ms, "plan": plan_ms, "census_kernels": census_ms,
                           "bin_kernels": [float(x) for x in avg_k],
                           "census_arcs_per_s": m_arcs / ((plan_ms + census_ms) * 1e-3)},
@@ -405,13 +454,27 @@ def run_ours(args):
         line["cpu_baseline_note"] = ("device-generated config: the oracle would need the "
                                      "1e9-arc graph on the host; see the C3 line")
     elif world == 1 and not args.no_cpu_baseline:
-        r = oracle_rate(a, args.cpu_seconds, steps=3)
+        cpu = host_cpu()
+        procs = max(1, min(cpu["affinity"], 64))
+        r = oracle_full_census(a, procs, budget_s=args.cpu_seconds)
+        gold = golden_census(args.config)
+        if r["full"]:
+            sample = ("one full census measured: oracle graph build (%.2f s, 1 core) + the "
+                      "census as %d equal-cost canonical-dyad ranges in %d forked "
+                      "single-threaded oracle processes (%.2f s wall, %.1f CPU-s)" %
+                      (r["t_build_s"], r["ranges"], procs, r["wall_s"], r["cpu_s"]))
+        else:
+            sample = ("oracle graph build (%.2f s) + %d of %d equal-cost canonical-dyad ranges "
+                      "(a systematic sample, %.1f%% of sum(|N(u)|+|N(v)|)) in %d forked "
+                      "processes, extrapolated linearly in that work unit" %
+                      (r["t_build_s"], r["ranges_run"], r["ranges"], 100 * r["work_frac"], procs))
         line["cpu_baseline"] = {
-            "value": r["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "oracle graph build once (%.1f s) + 3 contiguous canonical-dyad range "
-                      "censuses covering %.1f%% of sum(|N(u)|+|N(v)|), extrapolated linearly "
-                      "to the full census (%.1f s est.)" % (r["t_build_s"], 100 * r["sample_frac"],
-                                                             r["t_full_s"])}
+            "value": r["value"], "unit": UNIT, "cores": procs, "kind": "oracle",
+            "sample": sample, "measured_full_census": r["full"],
+            "census_matches_gpu": (r["census"] == ref_counts) if r["full"] else None,
+            "census_matches_golden": (r["census"] == gold) if (r["full"] and gold) else None,
+            "single_thread_equivalent_s": r["t_build_s"] + r["cpu_s"] / r["work_frac"],
+            "host": cpu}
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -419,8 +482,34 @@ def run_ours(args):
     return 0
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N ranks on this node with
+    torch.distributed.run (rendezvous on 127.0.0.1), never fall back to one
+    GPU.  The ranks inherit stdout: rank 0 prints the JSON line."""
+    import socket
+    if not args_impl_is_reference():
+        import torch
+        if torch.cuda.device_count() < n:
+            print("bench.py --gpus %d: only %d CUDA device(s) visible"
+                  % (n, torch.cuda.device_count()), file=sys.stderr)
+            return 2
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def args_impl_is_reference():
+    return "--impl" in sys.argv and sys.argv[sys.argv.index("--impl") + 1:][:1] == ["reference"]
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(args.gpus)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

@@ -19,46 +19,20 @@ number from ``oracle/``.
 """
 import argparse
 import json
-import multiprocessing as mp
 import os
 import sys
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 
-import numpy as np  # noqa: E402
-
 import oracle  # noqa: E402
 import synth  # noqa: E402
+from oracle import sharded  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-KAPPA = 8          # per-dyad constant of the cost model (entry equivalents)
-
-_G = None          # the oracle graph, built once in the parent and shared by fork
-
-
-def _work(rng):
-    b, e = rng
-    t0 = time.time()
-    part = _G.census_range(b, e)
-    return b, e, part, time.time() - t0
-
-
-def equal_cost_ranges(cost: np.ndarray, chunks: int):
-    """R contiguous ranges of [0, D) with about equal sum(cost + KAPPA)."""
-    D = cost.size
-    pre = np.cumsum(cost.astype(np.uint64) + np.uint64(KAPPA))
-    tot = int(pre[-1]) if D else 0
-    cuts = [0]
-    for r in range(1, chunks):
-        cuts.append(int(np.searchsorted(pre, tot * r // chunks, side="right")))
-    cuts.append(D)
-    cuts = sorted(set(cuts))
-    return [(cuts[i], cuts[i + 1]) for i in range(len(cuts) - 1) if cuts[i + 1] > cuts[i]]
 
 
 def main():
-    global _G
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 1)
@@ -67,9 +41,9 @@ def main():
     for name in args.configs:
         t_start = time.time()
         a = synth.make_config(name)
-        _G = oracle.Graph(a.n, a.src, a.dst)
-        st = _G.stats()
-        ranges = equal_cost_ranges(_G.dyad_costs(), args.chunks)
+        g = oracle.Graph(a.n, a.src, a.dst)
+        st = g.stats()
+        ranges = sharded.equal_cost_ranges(g.dyad_costs(), args.chunks)
         cache = os.path.join(HERE, "census_%s.partials.jsonl" % name)
         done = {}
         if os.path.exists(cache):
@@ -82,31 +56,27 @@ def main():
               % (name, a.n, st["m"], st["dyads"], len(ranges), len(ranges) - len(todo), args.procs),
               flush=True)
         cpu_s = sum(r["seconds"] for r in done.values())
-        with mp.get_context("fork").Pool(args.procs) as pool, open(cache, "a") as f:
-            for b, e, part, sec in pool.imap_unordered(_work, todo):
+        with open(cache, "a") as f:
+            def record(b, e, part, sec):
                 rec = {"begin": b, "end": e, "partial": [str(x) for x in part],
                        "seconds": round(sec, 2)}
                 f.write(json.dumps(rec) + "\n")
                 f.flush()
                 done[(b, e)] = rec
-                cpu_s += sec
                 print("  [%d/%d] %d..%d %.1fs" % (len(done), len(ranges), b, e, sec), flush=True)
-        total = [0] * 16
-        parts = []
-        for b, e in ranges:
-            p = [int(x) for x in done[(b, e)]["partial"]]
-            assert p[0] == 0
-            total = [x + y for x, y in zip(total, p)]
-            parts.append({"begin": b, "end": e, "partial": [str(x) for x in p]})
-        total[0] = oracle.choose3(a.n) - sum(total[1:])
+            _, _, cpu = sharded.census_ranges(g, todo, args.procs, record)
+        cpu_s += cpu
+        parts = [[int(x) for x in done[r]["partial"]] for r in ranges]
+        total = sharded.close(a.n, parts)
         rec = {"config": name, "label": a.meta["label"], "generator": a.meta["generator"],
                "seed": a.meta["seed"], "n": a.n, "m_drawn": a.m, "stats": st,
                "census": [str(x) for x in total], "classes": list(oracle.CLASS_NAMES),
                "oracle_seconds": round(time.time() - t_start, 2),
                "oracle_cpu_seconds": round(cpu_s, 2),
-               "sharding": {"ranges": len(ranges), "procs": args.procs, "kappa": KAPPA,
+               "sharding": {"ranges": len(ranges), "procs": args.procs, "kappa": sharded.KAPPA,
                             "cost": "d_u + d_v + kappa per canonical dyad (P:1693)"},
-               "range_partials": parts,
+               "range_partials": [{"begin": b, "end": e, "partial": [str(x) for x in p]}
+                                  for (b, e), p in zip(ranges, parts)],
                "written_by": "tests/golden/make_golden_sharded.py (oracle/ only)"}
         with open(os.path.join(HERE, "census_%s.json" % name), "w") as f:
             json.dump(rec, f, indent=1)
