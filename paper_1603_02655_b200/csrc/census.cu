@@ -193,6 +193,142 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     }
 }
 
+// measured slower (C3 thread bin 1.49 ms at 54 registers, 1.03 ms capped at
+// 48; the shared table: 0.87 ms): the trip loop is issue-bound, and the
+// 64-bit variable shift + selects cost more issue slots than one LDS.64
+#ifndef TC_THREAD_REGTAB
+#define TC_THREAD_REGTAB 0
+#endif
+
+// Thread bin, TriadTable out of the trip loop (SURVEY.md 8(a) "Table in
+// registers"): a canonical trip counts its tag pair, not its class -- nibble
+// idx = tu | tv << 2 of a per-thread uint64 (no shared-memory load, no bank
+// conflicts); nibble 0 (tu = tv = 0 never occurs in a canonical trip) counts
+// the non-canonical intersection elements u < w < v (own I).  Every <= 15
+// trips the nibbles move to 8-bit counters of the dyad's pre (three pairs of
+// uint64: even / odd idx); the warp flush (every <= 255 trips per lane) maps
+// (pre, idx) to the class TriadTable[pre | tu << 2 | tv << 4] and,
+// for idx with tu, tv != 0 (canonical intersection elements w > v), adds the
+// dyad's own I and the owed dyadic triad (class 102 if tv == 3, else 012).
+#if TC_THREAD_REGTAB
+struct AccT {
+    uint64_t n4;                     // nibble idx: canonical trips with tags idx
+    uint64_t e1, o1, e2, o2, e3, o3; // bytes: pre p, even idx / odd idx (byte idx >> 1)
+    uint32_t pending;
+    uint64_t dy012, dy102;
+};
+
+__device__ __forceinline__ void acct_init(AccT &c) {
+    c.n4 = c.e1 = c.o1 = c.e2 = c.o2 = c.e3 = c.o3 = 0;
+    c.pending = 0;
+    c.dy012 = c.dy102 = 0;
+}
+
+__device__ __forceinline__ void acct_spill(AccT &c, uint32_t pre) {
+    const uint64_t own = c.n4 & 15u;            // non-canonical intersections
+    if (pre == 3u) c.dy102 += own;
+    else c.dy012 += own;
+    const uint64_t E = c.n4 & (kNib & ~0xFull), O = (c.n4 >> 4) & kNib;
+    c.e1 += pre == 1u ? E : 0ull;
+    c.o1 += pre == 1u ? O : 0ull;
+    c.e2 += pre == 2u ? E : 0ull;
+    c.o2 += pre == 2u ? O : 0ull;
+    c.e3 += pre == 3u ? E : 0ull;
+    c.o3 += pre == 3u ? O : 0ull;
+    c.n4 = 0;
+}
+
+template <uint32_t P>
+__device__ __forceinline__ void acct_flush_pre(uint64_t &e, uint64_t &o, uint32_t lane,
+                                               unsigned long long *wsh) {
+    if (!__any_sync(0xffffffffu, (e | o) != 0ull)) return;
+#pragma unroll
+    for (uint32_t idx = 1; idx < 16; idx++) {
+        const uint32_t x = (uint32_t)(((idx & 1u) ? o : e) >> (8u * (idx >> 1))) & 255u;
+        const uint32_t sum = __reduce_add_sync(0xffffffffu, x);
+        if (lane == 0 && sum) {
+            const uint32_t tu = idx & 3u, tv = idx >> 2;
+            wsh[c_triad_table[P | idx << 2]] += sum;
+            if (tu && tv) {
+                wsh[P == 3u ? 2 : 1] += sum;     // own I of dyad (u, v)
+                wsh[tv == 3u ? 2 : 1] += sum;    // owed to dyad (v, w)
+            }
+        }
+    }
+    e = o = 0;
+}
+
+__device__ __forceinline__ void acct_flush(AccT &c, unsigned long long *wsh) {
+    const uint32_t lane = threadIdx.x & 31;
+    acct_flush_pre<1u>(c.e1, c.o1, lane, wsh);
+    acct_flush_pre<2u>(c.e2, c.o2, lane, wsh);
+    acct_flush_pre<3u>(c.e3, c.o3, lane, wsh);
+    c.pending = 0;
+}
+
+__device__ __forceinline__ void acct_reserve(AccT &c, unsigned long long *wsh, uint32_t len) {
+    if (__any_sync(0xffffffffu, c.pending + len > 255u)) acct_flush(c, wsh);
+    c.pending += len;
+}
+
+// thread-bin merge of a whole dyad: A = adj[pa..), B = adj[pb..), t trips
+__device__ __forceinline__ void merge_thread_reg(const uint32_t *__restrict__ adj, uint32_t pa,
+                                                 uint32_t pb, uint32_t kv, uint32_t pre,
+                                                 uint32_t t1, AccT &c) {
+    uint32_t lastA = 0u;
+    uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
+    uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
+    uint32_t t = 0;
+    while (t < t1) {
+        const uint32_t lim = min(t1, t + 15u);   // nibble counters hold 15
+#pragma unroll 2
+        for (; t < lim; t++) {
+            const uint32_t kx = x | 3u, ky = y | 3u;
+            const bool ta = kx <= ky;            // consume A (ties: A first)
+            const bool tb = ky <= kx;            // B's id is the merged id
+            const uint32_t ca = ta ? ((x & 3u) << 2) : 0u;    // 4 tu
+            const uint32_t cb = tb ? ((y & 3u) << 4) : 0u;    // 16 tv
+            const bool canon = ta ? (kx > kv) : (ky != lastA);
+            const uint32_t sh = canon ? (ca | cb) : 0u;       // 4 idx, or nibble 0
+            c.n4 += (canon || (ta && tb)) ? (1ull << sh) : 0ull;
+            lastA = ta ? kx : lastA;
+            pa += ta;
+            pb += !ta;
+            const uint32_t nv = __ldg(adj + (ta ? pa : pb) + 1u);
+            x = ta ? xn : x;
+            xn = ta ? nv : xn;
+            y = ta ? y : yn;
+            yn = ta ? yn : nv;
+        }
+        acct_spill(c, pre);
+    }
+}
+
+__device__ __forceinline__ void block_finish_t(AccT &c, unsigned long long (*wsh)[16],
+                                               unsigned long long *d_counts) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    acct_flush(c, wsh[warp]);
+    unsigned long long d0 = c.dy012, d1 = c.dy102;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        d0 += __shfl_xor_sync(0xffffffffu, d0, o);
+        d1 += __shfl_xor_sync(0xffffffffu, d1, o);
+    }
+    if (lane == 0) {
+        wsh[warp][1] += d0;
+        wsh[warp][2] += d1;
+    }
+    __syncthreads();
+    if (threadIdx.x >= 1 && threadIdx.x < 16) {
+        unsigned long long s = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; w++) s += wsh[w][threadIdx.x];
+        if (s) atomicAdd(&d_counts[threadIdx.x], s);
+    }
+}
+
+#endif  // TC_THREAD_REGTAB
+
 // shared increment tables: thread bin: 128 entries (canonical << 6 | code);
 // warp bin: 64 entries (pre << 4 | tu | tv << 2), canonical trips only; code = pre | tu << 2 | tv << 4: one nibble at 4 * class, and,
 // both tags set (an intersection element w > v), nibble 0 (own I) plus one
@@ -290,16 +426,26 @@ __device__ __forceinline__ uint64_t next_unit(unsigned long long *cursor, uint32
 // kPlanTile consecutive canonical dyads; inside a tile the plan ordered the
 // thread-bin dyads by merge length, so each warp's lanes run equal trip
 // counts while the tile keeps the N(u) rows of nearby u hot in L1/L2.
-__global__ void __launch_bounds__(kCensusThreads)
+#ifndef TC_THREAD_MINB
+#define TC_THREAD_MINB 1
+#endif
+__global__ void __launch_bounds__(kCensusThreads, TC_THREAD_MINB)
 k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__ tile_count,
                 uint64_t ntiles, const uint32_t *__restrict__ adj, unsigned long long *d_counts,
                 unsigned long long *cursor, uint32_t upt) {
-    __shared__ unsigned long long tab_s[128];
     __shared__ unsigned long long wsh[kWarps][16];
+#if TC_THREAD_REGTAB
+    for (int i = threadIdx.x; i < kWarps * 16; i += blockDim.x) (&wsh[0][0])[i] = 0;
+    __syncthreads();
+    AccT c;
+    acct_init(c);
+#else
+    __shared__ unsigned long long tab_s[128];
     block_setup<false>(tab_s, wsh);
     const uint32_t tab = (uint32_t)__cvta_generic_to_shared(tab_s);
     Acc c;
     acc_init(c);
+#endif
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t unit_s;
     const uint32_t unit_dyads = kPlanTile / upt;
@@ -323,11 +469,19 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
                 e.t &= 0xffffu;
                 prefetch_row_l2(adj, e.pb, e.t - alen);
             }
+#if TC_THREAD_REGTAB
+            acct_reserve(c, wsh[warp], e.t);
+            if (valid) merge_thread_reg(adj, e.pa, e.pb, e.e | 3u, e.e & 3u, e.t, c);
+        }
+    }
+    block_finish_t(c, wsh, d_counts);
+#else
             warp_reserve(c, wsh[warp], e.t);
             if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
         }
     }
     block_finish(c, wsh, d_counts);
+#endif
 }
 
 // warp bin: a warp takes the next item from a global cursor (dynamic, so

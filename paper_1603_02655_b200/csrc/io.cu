@@ -26,22 +26,47 @@
 
 namespace {
 
+// Line reader over 4 MB block reads (fread), not per-character stdio calls.
 struct Reader {
     FILE *f = nullptr;
     std::string line;
     uint64_t lineno = 0;
+    std::vector<char> buf = std::vector<char>(4 << 20);
+    size_t pos = 0, end = 0;
+    bool eof = false;
+    bool fill() {
+        if (eof) return false;
+        end = fread(buf.data(), 1, buf.size(), f);
+        pos = 0;
+        if (end == 0) eof = true;
+        return end > 0;
+    }
     bool next() {
         line.clear();
-        int ch;
         bool any = false;
-        while ((ch = fgetc(f)) != EOF) {
+        for (;;) {
+            if (pos == end && !fill()) break;
+            const char *b = buf.data() + pos;
+            const char *nl = (const char *)memchr(b, '\n', end - pos);
+            const size_t len = nl ? (size_t)(nl - b) : end - pos;
+            line.append(b, len);
             any = true;
-            if (ch == '\n') break;
-            if (ch != '\r') line.push_back((char)ch);
+            pos += len;
+            if (nl) {
+                pos++;   // the newline
+                break;
+            }
         }
         if (!any) return false;
+        if (!line.empty() && line.back() == '\r') line.pop_back();
         lineno++;
         return true;
+    }
+    void rewind_file() {
+        rewind(f);
+        pos = end = 0;
+        eof = false;
+        lineno = 0;
     }
 };
 
@@ -210,8 +235,7 @@ tc_status tc_read_arcs(const char *path, int format, int index_base, uint64_t *n
             format = (*p == '*') ? 1 : 2;
             break;
         }
-        rewind(r.f);
-        r.lineno = 0;
+        r.rewind_file();
     }
     tc_status st = format == 1 ? read_pajek(r, n, src, dst, m)
                                : read_edgelist(r, index_base, n, src, dst, m);

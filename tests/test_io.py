@@ -62,3 +62,47 @@ def test_pajek_round_trip_census(tcb, tmp_path):
     n, s, d = tcb.tc_read_arcs(write(tmp_path, "r.net", "\n".join(lines) + "\n"))
     assert n == a.n and arcs(s, d) == arcs(a.src, a.dst)
     assert oracle.census(n, s, d) == oracle.census(a.n, a.src, a.dst)
+
+
+def _write_snap(path, a, base):
+    with open(path, "w") as f:
+        f.write("# Directed graph (each unordered pair a line)\n# FromNodeId\tToNodeId\n")
+        np.savetxt(f, np.stack([a.src.astype(np.int64) + base, a.dst.astype(np.int64) + base], 1),
+                   fmt="%d", delimiter="\t")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("fmt", ["pajek", "snap0", "snap1"])
+def test_census_file_gpu_vs_oracle(tmp_path, fmt):
+    # f2 end to end on the GPU: file -> native reader -> CUDA census, against
+    # the oracle on the generator's own arcs; the paper's phase breakdown
+    # (read graph / neighbour sets / task queues / census) is
+    # reported
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1603_02655_b200 as tcb
+    a = synth.make_config("C2")
+    if fmt == "pajek":
+        p = str(tmp_path / "c2.net")
+        half = a.src.size // 2           # second half as *Edges (each -> two arcs)
+        with open(p, "w") as f:
+            f.write("*Vertices %d\n*Arcs\n" % a.n)
+            np.savetxt(f, np.stack([a.src[:half] + 1, a.dst[:half] + 1], 1).astype(np.int64),
+                       fmt="%d")
+            f.write("*Edges\n")
+            np.savetxt(f, np.stack([a.src[half:] + 1, a.dst[half:] + 1], 1).astype(np.int64),
+                       fmt="%d")
+        src = np.concatenate([a.src, a.dst[half:]])
+        dst = np.concatenate([a.dst, a.src[half:]])
+        n = a.n
+    else:
+        base = int(fmt[-1])
+        p = str(tmp_path / "c2.txt")
+        _write_snap(p, a, base)
+        src, dst = a.src, a.dst
+        n = int(max(a.src.max(), a.dst.max())) + 1      # SNAP: n = max id - base + 1
+    counts, timing = tcb.census_file(p, index_base=None if fmt == "pajek" else int(fmt[-1]))
+    assert counts == oracle.census(n, src, dst)
+    for k in ("read_graph", "build_csr", "plan", "census_kernels", "total"):
+        assert timing[k] >= 0.0
