@@ -412,11 +412,25 @@ def run_ours(args):
     names = ["k_census_thread", "k_census_warp"]
     if args.mode == "64":
         names = ["k_census_thread64", "k_census_warp64"]
-    traffic = None
+    traffic, traffic_src = None, None
     tp = os.path.join(ROOT, "profiles", "traffic_%s.json" % args.config)
     if os.path.exists(tp):
         tr = json.load(open(tp))
         traffic = tr.get(names[dom])
+        traffic_src = ("profiles/traffic_%s.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                       "per launch from a committed ncu --set full capture (%s), not measured in "
+                       "this run" % (args.config, tr.get("_source", "see profiles/")))
+    # bytes the dominant kernel's merges touch (merge trips over the entries
+    # w > u, reading 21) + the per-dyad 24 B -- below B_alg
+    trips = int(profs[-1]["bin_work"][2 + dom])
+    touched = 4.0 * (trips + (sp_units if dom == 1 else 0)) + 24.0 * items
+    # a1 build: compulsory bytes (read the arcs once, write the CSR, the five
+    # dyad arrays, off and ups) and the sort traffic of the passes it runs
+    nb = max(1, int(np.ceil(np.log2(max(a.n, 2)))))
+    passes_m, passes_d = 2 * ((nb + 7) // 8), (nb + 7) // 8
+    m_, d_ = stats["m_in"], stats["dyads"]
+    compulsory = 8.0 * m_ + 4.0 * (2 * d_ + a.n) + 20.0 * d_ + 8.0 * a.n
+    sort_bytes = 24.0 * (passes_m * m_ + passes_d * d_)
     census_ms = float(np.mean([p["census_ms"] for p in profs]))
     plan_ms = float(np.mean([p["plan_ms"] for p in profs]))
     build_ms = float(np.mean([p["build_ms"] for p in profs]))
@@ -438,12 +452,30 @@ def run_ours(args):
                      "bin_merge_trips": [int(profs[-1]["bin_work"][2]),
                                          int(profs[-1]["bin_work"][3])]},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "kernel": names[dom],
+                         "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": names[dom],
                          "bytes_alg_per_launch": bytes_alg,
+                         "bytes_alg_model": "SURVEY 8(d) B-M model: 4 (d_u + d_v) + 24 B per "
+                                            "merged dyad (skewed pairs: 4 (s ceil(log2(l+1)) "
+                                            "+ 4) + 24), not the bytes the kernel reads",
+                         "touched_bytes_per_launch": touched,
+                         "touched_frac": (touched / (avg_k[dom] * 1e-3) / 1e9) / hbm,
+                         "dram_frac": ((traffic / (avg_k[dom] * 1e-3) / 1e9) / hbm)
+                         if traffic else None,
                          "skewed_pair_dyads": sp_dyads,
                          "merge_equivalent_frac": (bytes_merge_equiv / (avg_k[dom] * 1e-3) / 1e9) / hbm,
                          "peak_source": peak_src,
                          "all_bins_frac": (sum_all_bins_bytes / (sum(avg_k) * 1e-3) / 1e9) / hbm},
+            "build_roofline": {
+                "bound": "hbm", "build_ms": build_ms, "peak": hbm, "unit": "GB/s",
+                "compulsory_bytes": compulsory,
+                "compulsory_frac": (compulsory / (build_ms * 1e-3) / 1e9) / hbm,
+                "sort_passes": {"over_m_keys": passes_m, "over_D_keys": passes_d},
+                "sort_bytes": sort_bytes,
+                "sort_gbps_if_all_time": sort_bytes / (build_ms * 1e-3) / 1e9,
+                "model": "compulsory = 8m (arcs) + 4(2D+n) (adj) + 20D (dyad arrays) + 8n "
+                         "(off, ups); sort = 24 B per key per LSD pass (upsweep read + "
+                         "downsweep read + write)"},
             "e2e": {"value": m_arcs * args.steps / (e2e_total * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 8 * a_m, "d2h_bytes_per_step": 320},
             "gpu_launches": launches_total,
