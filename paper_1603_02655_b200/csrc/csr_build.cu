@@ -82,15 +82,40 @@ __device__ __forceinline__ uint32_t key_row(uint64_t k) { return (uint32_t)(k >>
 __device__ __forceinline__ uint32_t key_col(uint64_t k) { return (uint32_t)((k >> 2) & 0x3fffffffu); }
 __device__ __forceinline__ uint32_t swap_tag(uint32_t t) { return ((t & 1u) << 1) | (t >> 1); }
 
-// key i (warp-striped: lanes hold consecutive keys), its predecessor, and
-// whether it starts a (row, col) run
-__device__ __forceinline__ void run_head(const uint64_t *__restrict__ key, size_t L, size_t i,
-                                         uint64_t &k, uint64_t &prev, bool &head) {
+// The warp's 512 keys (iteration r holds keys base + 32 r + lane), all loaded
+// before use (16 loads in flight per lane), plus the key before the chunk
+// (lane 0) and the key after it (lane 31).
+struct HeadChunk {
+    uint64_t k[kHcItems];
+    uint64_t before, after;
+};
+
+__device__ __forceinline__ void load_chunk(const uint64_t *__restrict__ key, size_t L, size_t base,
+                                           HeadChunk &c) {
     const uint32_t lane = threadIdx.x & 31;
-    k = i < L ? __ldg(key + i) : kSentinel;
+#pragma unroll
+    for (int r = 0; r < kHcItems; r++) {
+        const size_t i = base + (size_t)r * 32 + lane;
+        c.k[r] = i < L ? __ldg(key + i) : kSentinel;
+    }
+    c.before = (lane == 0 && base > 0 && base - 1 < L) ? __ldg(key + base - 1) : kSentinel;
+    const size_t ia = base + 32 * kHcItems;
+    c.after = (lane == 31 && ia < L) ? __ldg(key + ia) : kSentinel;
+}
+
+// iteration r: key, predecessor, successor, and whether it starts a (row,
+// col) run (all lanes must call it: shuffles)
+__device__ __forceinline__ bool chunk_head(const HeadChunk &c, int r, size_t L, size_t i,
+                                           uint64_t &k, uint64_t &prev, uint64_t &nxt) {
+    const uint32_t lane = threadIdx.x & 31;
+    k = c.k[r];
     prev = __shfl_up_sync(0xffffffffu, k, 1);
-    if (lane == 0) prev = (i > 0 && i - 1 < L) ? __ldg(key + i - 1) : kSentinel;
-    head = i < L && (i == 0 || (prev >> 2) != (k >> 2));
+    const uint64_t pl = __shfl_sync(0xffffffffu, c.k[r > 0 ? r - 1 : 0], 31);
+    if (lane == 0) prev = r > 0 ? pl : c.before;
+    nxt = __shfl_down_sync(0xffffffffu, k, 1);
+    const uint64_t nf = __shfl_sync(0xffffffffu, c.k[r < kHcItems - 1 ? r + 1 : r], 0);
+    if (lane == 31) nxt = r < kHcItems - 1 ? nf : c.after;
+    return i < L && (i == 0 || (prev >> 2) != (k >> 2));
 }
 
 // pass 1: per warp (512 keys), number of run heads
@@ -100,12 +125,13 @@ k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
     const size_t L = m - *dropped;   // canonical keys (dropped arcs sort last)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
+    HeadChunk c;
+    load_chunk(key, L, base, c);
     uint32_t nh = 0;
-#pragma unroll 4
+#pragma unroll
     for (int r = 0; r < kHcItems; r++) {
-        uint64_t k, prev;
-        bool head;
-        run_head(key, L, base + (size_t)r * 32 + lane, k, prev, head);
+        uint64_t k, prev, nxt;
+        const bool head = chunk_head(c, r, L, base + (size_t)r * 32 + lane, k, prev, nxt);
         nh += __popc(__ballot_sync(0xffffffffu, head));
     }
     if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = nh;
@@ -124,15 +150,14 @@ k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
     const uint32_t lt = (1u << lane) - 1u;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
     uint32_t k0 = warp_off[(size_t)blockIdx.x * kHcWarps + warp];
+    HeadChunk c;
+    load_chunk(key, L, base, c);
+#pragma unroll
     for (int r = 0; r < kHcItems; r++) {
         const size_t i = base + (size_t)r * 32 + lane;
-        uint64_t k, prev;
-        bool head;
-        run_head(key, L, i, k, prev, head);
+        uint64_t k, prev, nxt;
+        const bool head = chunk_head(c, r, L, i, k, prev, nxt);
         const uint32_t bh = __ballot_sync(0xffffffffu, head);
-        // next key (lane + 1, or a load for lane 31) for the run's tag OR
-        uint64_t nxt = __shfl_down_sync(0xffffffffu, k, 1);
-        if (lane == 31) nxt = i + 1 < L ? __ldg(key + i + 1) : kSentinel;
         if (head) {
             const uint32_t kk = k0 + __popc(bh & lt);
             const uint32_t row = key_row(k), col = key_col(k);
@@ -170,20 +195,44 @@ k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
 // The same pass records lo_start[x] = first index of row x among the
 // row-sorted transposed keys (rows with no lower entries get the next row's
 // start; the rows after the last one are filled by k_fill_tail_last).
+// Each thread takes kWlBatch keys (grid-strided) and issues all their loads --
+// the keys, up_start of their rows, the random ul[k] -- before any store, so
+// the random L2 round trips overlap instead of serialising behind the
+// (possibly aliasing) ul[k] stores of the previous key.
+constexpr int kWlBatch = 4;
 __global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
                               const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
                               uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start) {
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < D;
-         i += (size_t)gridDim.x * blockDim.x) {
-        const uint64_t key = __ldg(tk + i);
-        const uint32_t r = key_row(key), k = (uint32_t)key;
-        const uint32_t pos = __ldg(up_start + r) + r + (uint32_t)i;
-        adj[pos] = ul[k];
-        ul[k] = pos + 1u;
-        const uint32_t prev = i ? key_row(__ldg(tk + i - 1)) : 0xffffffffu;
-        if (i == 0 || prev != r) {
-            const uint32_t first = i == 0 ? 0u : prev + 1;
-            for (uint32_t x = first; x <= r; x++) lo_start[x] = (uint32_t)i;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < D;
+         i0 += kWlBatch * stride) {
+        uint64_t key[kWlBatch], prv[kWlBatch];
+        uint32_t us[kWlBatch], val[kWlBatch];
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const size_t i = i0 + j * stride;
+            key[j] = i < D ? __ldg(tk + i) : 0ull;
+            prv[j] = (i < D && i) ? __ldg(tk + i - 1) : ~0ull;
+        }
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const size_t i = i0 + j * stride;
+            us[j] = i < D ? __ldg(up_start + key_row(key[j])) : 0u;
+            val[j] = i < D ? ul[(uint32_t)key[j]] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const size_t i = i0 + j * stride;
+            if (i >= D) continue;
+            const uint32_t r = key_row(key[j]), k = (uint32_t)key[j];
+            const uint32_t pos = us[j] + r + (uint32_t)i;
+            adj[pos] = val[j];
+            ul[k] = pos + 1u;
+            const uint32_t prev = i ? key_row(prv[j]) : 0xffffffffu;
+            if (i == 0 || prev != r) {
+                const uint32_t first = i == 0 ? 0u : prev + 1;
+                for (uint32_t x = first; x <= r; x++) lo_start[x] = (uint32_t)i;
+            }
         }
     }
 }
@@ -261,16 +310,42 @@ __global__ void k_write_upper(const uint32_t *__restrict__ off, const uint32_t *
                               uint32_t *__restrict__ adj, uint32_t *__restrict__ dc,
                               uint32_t *__restrict__ dt, unsigned long long *out) {
     unsigned long long m = 0, mu = 0;
-    for (uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k < D;
-         k += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t u = du[k], e = de[k], v = e >> 2, t = e & 3u;
-        adj[__ldg(lo_start + u + 1) + u + (uint32_t)k] = e;
-        const uint32_t ou = __ldg(off + u), ou1 = __ldg(off + u + 1);
-        const uint32_t ov = __ldg(off + v), ov1 = __ldg(off + v + 1);
-        dc[k] = (ou1 - ou) + (ov1 - ov) - 2;
-        dt[k] = (ou1 - 1 - __ldg(ups + u)) + (ov1 - 1 - dpb[k]);
-        m += __popc(t);
-        mu += (t == 3u);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // kWlBatch dyads per thread, all loads (the random off[v], off[v+1] among
+    // them) issued before the stores
+    for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < D;
+         k0 += kWlBatch * stride) {
+        uint32_t u[kWlBatch], e[kWlBatch], pb[kWlBatch], ls[kWlBatch], ou[kWlBatch],
+            ou1[kWlBatch], ov[kWlBatch], ov1[kWlBatch], up[kWlBatch];
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const uint64_t k = k0 + j * stride;
+            const bool ok = k < D;
+            u[j] = ok ? __ldg(du + k) : 0u;
+            e[j] = ok ? __ldg(de + k) : 0u;
+            pb[j] = ok ? dpb[k] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const uint32_t v = e[j] >> 2;
+            ls[j] = __ldg(lo_start + u[j] + 1);
+            ou[j] = __ldg(off + u[j]);
+            ou1[j] = __ldg(off + u[j] + 1);
+            up[j] = __ldg(ups + u[j]);
+            ov[j] = __ldg(off + v);
+            ov1[j] = __ldg(off + v + 1);
+        }
+#pragma unroll
+        for (int j = 0; j < kWlBatch; j++) {
+            const uint64_t k = k0 + j * stride;
+            if (k >= D) continue;
+            adj[ls[j] + u[j] + (uint32_t)k] = e[j];
+            dc[k] = (ou1[j] - ou[j]) + (ov1[j] - ov[j]) - 2;
+            dt[k] = (ou1[j] - 1 - up[j]) + (ov1[j] - 1 - pb[j]);
+            const uint32_t t = e[j] & 3u;
+            m += __popc(t);
+            mu += (t == 3u);
+        }
     }
     m = warp_sum64(m);
     mu = warp_sum64(mu);

@@ -123,6 +123,49 @@ struct DownSmem {
     uint32_t gbase[kMaxRadix];               // global offset - local offset per digit
 };
 
+// the tile's keys of this warp (warp-striped: iteration k holds keys wbase +
+// 32 k + lane) and their stable ranks among the warp's keys of equal digit:
+// one ballot per digit bit groups the lanes holding the same digit, the
+// earlier peers plus the running per-warp count give the rank
+template <int BITS, bool ARCS, bool FULL>
+__device__ __forceinline__ void ds_load_rank(const uint64_t *__restrict__ keys, size_t n, int shift,
+                                             uint32_t mask, const ArcSource &a, size_t wbase,
+                                             uint16_t *wc, uint64_t (&key)[kDsItems],
+                                             uint32_t (&rank2)[kDsItems / 2]) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t lt = (1u << lane) - 1u;
+    // all 16 loads in flight before the first use (the ranking chain below
+    // is serial per warp)
+#pragma unroll
+    for (int k = 0; k < kDsItems; k++) {
+        const size_t i = wbase + (size_t)k * 32 + lane;
+        const bool valid = FULL || i < n;
+        if (ARCS) key[k] = valid ? arc_key(__ldcs(a.src + i), __ldcs(a.dst + i), a.nv) : 0ull;
+        else key[k] = valid ? __ldcs(keys + i) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < kDsItems; k++) {
+        const size_t i = wbase + (size_t)k * 32 + lane;
+        const bool valid = FULL || i < n;
+        const uint32_t d = valid ? ((uint32_t)(key[k] >> shift) & mask) : 0x10000u;
+        // lanes holding the same digit: intersect one ballot per digit bit
+        // (cheaper than __match_any_sync on sm_100)
+        uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bit = 0; bit < BITS; bit++) {   // only the digit's own bits
+            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+            peers &= ((d >> bit) & 1u) ? b : ~b;
+        }
+        uint32_t r = 0;
+        if (valid) r = wc[d] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[d] += __popc(peers);
+        __syncwarp();
+        if (k & 1) rank2[k >> 1] |= r << 16;
+        else rank2[k >> 1] = r;
+    }
+}
+
 template <int BITS, bool ARCS>
 __global__ void __launch_bounds__(kDsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
@@ -133,40 +176,16 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kDsWarps * radix; i += kDsThreads) S.wc[i / radix][i % radix] = 0;
     __syncthreads();
-    const uint32_t lt = (1u << lane) - 1u;
     const size_t tile0 = (size_t)blockIdx.x * kRsTile;
     const size_t wbase = tile0 + (size_t)warp * 32 * kDsItems;
     uint64_t key[kDsItems];
     uint32_t rank2[kDsItems / 2];      // two 16-bit ranks per register
-    // all 16 loads in flight before the first use (the ranking chain below
-    // is serial per warp)
-#pragma unroll
-    for (int k = 0; k < kDsItems; k++) {
-        size_t i = wbase + (size_t)k * 32 + lane;
-        if (ARCS) key[k] = i < n ? arc_key(__ldcs(a.src + i), __ldcs(a.dst + i), a.nv) : 0ull;
-        else key[k] = i < n ? __ldcs(keys + i) : 0ull;
-    }
-#pragma unroll
-    for (int k = 0; k < kDsItems; k++) {
-        size_t i = wbase + (size_t)k * 32 + lane;
-        bool valid = i < n;
-        uint32_t d = valid ? ((uint32_t)(key[k] >> shift) & mask) : 0x10000u;
-        // lanes holding the same digit: intersect one ballot per digit bit
-        // (cheaper than __match_any_sync on sm_100)
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bit = 0; bit < BITS; bit++) {   // only the digit's own bits
-            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-            peers &= ((d >> bit) & 1u) ? b : ~b;
-        }
-        uint32_t r = 0;
-        if (valid) r = S.wc[warp][d] + __popc(peers & lt);
-        __syncwarp();
-        if (valid && (peers & lt) == 0) S.wc[warp][d] += __popc(peers);
-        __syncwarp();
-        if (k & 1) rank2[k >> 1] |= r << 16;
-        else rank2[k >> 1] = r;
-    }
+    // every tile but the last is full: no per-key bounds checks or validity
+    // ballot there
+    if (tile0 + kRsTile <= n)
+        ds_load_rank<BITS, ARCS, true>(keys, n, shift, mask, a, wbase, S.wc[warp], key, rank2);
+    else
+        ds_load_rank<BITS, ARCS, false>(keys, n, shift, mask, a, wbase, S.wc[warp], key, rank2);
     __syncthreads();
     // tile-local digit offsets: exclusive scan over digits of the digit totals
     // (each thread owns radix/256 consecutive digits), then per-warp offsets

@@ -37,6 +37,13 @@ def main():
     ap.add_argument("configs", nargs="+")
     ap.add_argument("--procs", type=int, default=os.cpu_count() or 1)
     ap.add_argument("--chunks", type=int, default=256)
+    ap.add_argument("--reverse", action="store_true",
+                    help="run the uncached ranges last-first (a second host sharing the work)")
+    ap.add_argument("--cache", default=None,
+                    help="append finished ranges here (default: beside the output); "
+                         "ranges cached in either file are skipped")
+    ap.add_argument("--no-write", action="store_true",
+                    help="only fill the cache (another host writes the golden)")
     args = ap.parse_args()
     for name in args.configs:
         t_start = time.time()
@@ -44,14 +51,18 @@ def main():
         g = oracle.Graph(a.n, a.src, a.dst)
         st = g.stats()
         ranges = sharded.equal_cost_ranges(g.dyad_costs(), args.chunks)
-        cache = os.path.join(HERE, "census_%s.partials.jsonl" % name)
+        default_cache = os.path.join(HERE, "census_%s.partials.jsonl" % name)
+        cache = args.cache or default_cache
         done = {}
-        if os.path.exists(cache):
-            with open(cache) as f:
-                for line in f:
-                    r = json.loads(line)
-                    done[(r["begin"], r["end"])] = r
+        for c in {default_cache, cache}:
+            if os.path.exists(c):
+                with open(c) as f:
+                    for line in f:
+                        r = json.loads(line)
+                        done[(r["begin"], r["end"])] = r
         todo = [r for r in ranges if r not in done]
+        if args.reverse:
+            todo = todo[::-1]
         print("%s: n=%d m=%d D=%d, %d ranges (%d cached), %d procs"
               % (name, a.n, st["m"], st["dyads"], len(ranges), len(ranges) - len(todo), args.procs),
               flush=True)
@@ -66,6 +77,8 @@ def main():
                 print("  [%d/%d] %d..%d %.1fs" % (len(done), len(ranges), b, e, sec), flush=True)
             _, _, cpu = sharded.census_ranges(g, todo, args.procs, record)
         cpu_s += cpu
+        if args.no_write:
+            continue
         parts = [[int(x) for x in done[r]["partial"]] for r in ranges]
         total = sharded.close(a.n, parts)
         rec = {"config": name, "label": a.meta["label"], "generator": a.meta["generator"],
