@@ -44,6 +44,8 @@
 // uint64 of 8-bit counters (even / odd classes), which a warp flushes (REDUX
 // sum per class) into per-warp shared totals before they can overflow;
 // blocks end with one global atomicAdd per class.
+#include <atomic>
+
 #include "census.cuh"
 
 namespace tc {
@@ -790,23 +792,34 @@ k_census_warp64(const BinLists L, const uint32_t *__restrict__ off,
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
                       cudaEvent_t *ev, uint64_t *launches, int mode64) {
     unsigned long long *out = reinterpret_cast<unsigned long long *>(d_counts);
-    int sms = 148, per = 0, perw = 0;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+    // SM count and resident blocks per SM of the four bin kernels, queried
+    // once per device (host time between the plan and the bins is exposed)
+    struct Occ {
+        int sms, thread, warp, thread64, warp64;
+    };
+    static Occ occ[64];
+    static std::atomic<uint64_t> occ_done{0};
+    const int dv = g->device & 63;
+    if (!(occ_done.load() & (1ull << dv))) {
+        Occ o{148, 0, 0, 0, 0};
+        cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, g->device);
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.warp64, k_census_warp64,
+                                                              kCensusThreads, 0));
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.warp, k_census_warp,
+                                                              kCensusThreads, 0));
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.thread64, k_census_thread64,
+                                                              kCensusThreads, 0));
+        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.thread, k_census_thread,
+                                                              kCensusThreads, 0));
+        occ[dv] = o;
+        occ_done.fetch_or(1ull << dv);
+    }
+    const int sms = occ[dv].sms;
+    const int perw = mode64 ? occ[dv].warp64 : occ[dv].warp;
+    const int per = mode64 ? occ[dv].thread64 : occ[dv].thread;
     // warp bin: one resident wave, items handed out by bl.wcursor
-    if (mode64)
-        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perw, k_census_warp64,
-                                                              kCensusThreads, 0));
-    else
-        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perw, k_census_warp,
-                                                              kCensusThreads, 0));
     const unsigned grid = (unsigned)sms * (unsigned)(perw > 0 ? perw : 1);
     // thread bin: one resident wave, units handed out by bl.cursor
-    if (mode64)
-        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_census_thread64,
-                                                              kCensusThreads, 0));
-    else
-        TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_census_thread,
-                                                              kCensusThreads, 0));
     uint64_t tgrid = (uint64_t)sms * (per > 0 ? per : 1);
     const uint32_t upt = bl.ntiles >= 4 * tgrid ? 2u : 4u;   // units per plan tile
     const uint64_t units = bl.ntiles * upt;

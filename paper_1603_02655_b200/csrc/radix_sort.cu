@@ -12,6 +12,8 @@
 //              tile is reordered by digit in shared memory and written out
 //              so consecutive threads store consecutive addresses of each
 //              digit run (coalesced), instead of a 32-way scatter per warp.
+#include <atomic>
+
 #include "radix_sort.cuh"
 #include "scan.cuh"
 
@@ -252,10 +254,20 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         return TC_E_INVALID;
     }
     static const DownFn kDown[2][kMaxBits + 1] = {TC_DS(false), TC_DS(true)};
-    for (int a = 0; a < 2; a++)
-        for (int b = 1; b <= kMaxBits; b++)
-            TC_CUDA(cudaFuncSetAttribute(kDown[a][b], cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sizeof(DownSmem)));
+    // the shared-memory opt-in of the 16 downsweep instances, once per device
+    // (driver calls on every sort cost host time on the build's critical path)
+    static std::atomic<uint64_t> attr_done{0};
+    int dev = 0;
+    TC_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_done.load() & bit)) {
+        for (int a = 0; a < 2; a++)
+            for (int b = 1; b <= kMaxBits; b++)
+                TC_CUDA(cudaFuncSetAttribute(kDown[a][b],
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sizeof(DownSmem)));
+        attr_done.fetch_or(bit);
+    }
     const ArcSource none{nullptr, nullptr, 0, nullptr};
     size_t ntiles = (n + kRsTile - 1) / kRsTile;
     int maxbits = 1;
