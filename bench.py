@@ -515,23 +515,22 @@ def run_ours(args):
 
 
 def spawn_ranks(n):
-    """`bench.py --gpus N` without a launcher: start N ranks on this node with
-    torch.distributed.run (rendezvous on 127.0.0.1), never fall back to one
-    GPU.  The ranks inherit stdout: rank 0 prints the JSON line."""
-    import socket
+    """`bench.py --gpus N` without a launcher: start N ranks on this node
+    (paper_1603_02655_b200/launch.py: torch.distributed.run, rendezvous on
+    127.0.0.1), never fall back to one GPU.  The ranks inherit stdout: rank 0
+    prints the JSON line."""
     if not args_impl_is_reference():
         import torch
         if torch.cuda.device_count() < n:
             print("bench.py --gpus %d: only %d CUDA device(s) visible"
                   % (n, torch.cuda.device_count()), file=sys.stderr)
             return 2
-    with socket.socket() as sk:
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1", "--master-port", str(port),
-           os.path.abspath(__file__)] + sys.argv[1:]
-    return subprocess.call(cmd)
+    import importlib.util
+    spec = importlib.util.spec_from_file_location(
+        "tc_launch", os.path.join(ROOT, "paper_1603_02655_b200", "launch.py"))
+    launch = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(launch)
+    return launch.spawn_local(n, os.path.abspath(__file__), sys.argv[1:])
 
 
 def args_impl_is_reference():
