@@ -534,24 +534,54 @@ __device__ __forceinline__ uint32_t tag_in(const uint32_t *__restrict__ L, uint3
     return 0u;
 }
 
-__device__ __forceinline__ void sp_add(unsigned long long *sp, uint32_t cls,
-                                       unsigned long long x) {
+// skewed-pair class counts: per-warp uint32 shared counters (native 32-bit
+// shared atomics; 64-bit shared atomics are CAS loops on sm_100), added
+// modulo 2^32 (a take-back may precede its add) and moved, sign-extended,
+// into the warp's uint64 totals after every item (an item's net count per
+// class is below 2^31 in magnitude: <= 3 * 256 entries + one row's tags)
+#ifndef TC_SP_U32
+#define TC_SP_U32 1
+#endif
+#if TC_SP_U32
+typedef uint32_t sp_t;
+#else
+typedef unsigned long long sp_t;
+#endif
+__device__ __forceinline__ void sp_add(sp_t *sp, uint32_t cls, uint32_t x) {
+#if TC_SP_U32
     atomicAdd(&sp[cls], x);
+#else
+    atomicAdd(&sp[cls], (unsigned long long)(long long)(int32_t)x);
+#endif
+}
+
+__device__ __forceinline__ void sp_drain(sp_t *sp, unsigned long long *wsh) {
+    __syncwarp();
+    const uint32_t lane = threadIdx.x & 31;
+    if (lane < 16) {
+#if TC_SP_U32
+        wsh[lane] += (unsigned long long)(long long)(int32_t)sp[lane];
+#else
+        wsh[lane] += sp[lane];
+#endif
+        sp[lane] = 0;
+    }
+    __syncwarp();
 }
 
 __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__restrict__ P,
                             const WarpDyad &w, uint32_t mode, uint32_t d0, uint32_t d1,
-                            unsigned long long *sp) {
+                            sp_t *sp) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t v = w.e >> 2, pre = w.e & 3u;
-    const unsigned long long minus1 = ~0ull;
+    const uint32_t minus1 = ~0u;
     uint32_t own = 0, o012 = 0, o102 = 0;
     if (mode == 1u) {
         for (uint32_t j = d0 + lane; j < d1; j += 32) {
             const uint32_t x = __ldg(adj + w.oa + j), id = x >> 2, tu = x & 3u;
             if (id == v) continue;
             const uint32_t tv = tag_in(adj + w.ob, w.b, id);
-            if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1ull);
+            if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
             if (tv) {
                 own++;
                 if (id > v) {
@@ -573,11 +603,11 @@ __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__
             const uint32_t y = __ldg(adj + w.ob + j), id = y >> 2, tv = y & 3u;
             const uint32_t tu = tag_in(adj + w.oa, w.a, id);
             if (!tu) {
-                sp_add(sp, c_triad_table[pre | tv << 4], 1ull);
+                sp_add(sp, c_triad_table[pre | tv << 4], 1u);
             } else {
                 own++;
                 if (id > v) {
-                    sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1ull);
+                    sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
                     o102 += tv == 3u;
                     o012 += tv != 3u;
                     sp_add(sp, c_triad_table[pre | tu << 2], minus1);
@@ -617,15 +647,16 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
     Acc c;
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __shared__ unsigned long long sp[16];   // skewed-pair class counts (wrapping)
-    if (threadIdx.x < 16) sp[threadIdx.x] = 0;
-    __syncthreads();
+    __shared__ sp_t spw[kWarps][16];   // skewed-pair class counts, per warp (wrapping)
+    if (lane < 16) spw[warp][lane] = 0;
+    __syncwarp();
     const uint64_t count = *L.w_count;
     for (uint64_t it = next_item(L.wcursor); it < count; it = next_item(L.wcursor)) {
         const BinItemW e = L.w[it];
         const WarpDyad w = warp_dyad(L, off, ups, e.k);
         if (e.pad) {   // warp-uniform
-            sparse_item(adj, L.tagpre, w, e.pad, e.d0, e.d1, sp);
+            sparse_item(adj, L.tagpre, w, e.pad, e.d0, e.d1, spw[warp]);
+            sp_drain(spw[warp], wsh[warp]);
             continue;
         }
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
@@ -634,8 +665,6 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
         if (d0 < d1) merge_diag<true>(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
     }
     block_finish(c, wsh, d_counts);
-    if (threadIdx.x >= 1 && threadIdx.x < 16 && sp[threadIdx.x])
-        atomicAdd(&d_counts[threadIdx.x], sp[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------------------
