@@ -144,7 +144,10 @@ __device__ __forceinline__ uint32_t merge_path(const uint32_t *__restrict__ A, u
 // both followed by more of their row and a sentinel; kv = v<<2|3; tab =
 // shared address of the 128-entry uint64 increment table.  The caller has
 // reserved d1 - d0 byte-counter increments (warp_reserve).
-template <bool PRED>
+// LA2: two elements of look-ahead per list instead of one (the load issued
+// at a trip is consumed two consumptions of that list later; two more
+// registers and selects per trip)
+template <bool PRED, bool LA2 = false>
 __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uint32_t oa,
                                            uint32_t a, uint32_t ob, uint32_t b, uint32_t kv,
                                            uint32_t pre, uint32_t d0, uint32_t d1, uint32_t tab,
@@ -153,9 +156,11 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
     if (d0 > 0) i = merge_path(adj + oa, a, adj + ob, b, d0);
     uint32_t pa = oa + i, pb = ob + (d0 - i);
     uint32_t lastA = i > 0 ? (__ldg(adj + pa - 1) | 3u) : 0u;
-    // current heads and the next elements (sentinel-terminated rows)
+    // current heads and the next elements (sentinel-terminated rows; the
+    // look-ahead may read past a sentinel into the next row or the slack)
     uint32_t x = __ldg(adj + pa), xn = __ldg(adj + pa + 1);
     uint32_t y = __ldg(adj + pb), yn = __ldg(adj + pb + 1);
+    uint32_t xnn = LA2 ? __ldg(adj + pa + 2) : 0u, ynn = LA2 ? __ldg(adj + pb + 2) : 0u;
     // canonical increments of this pre: 16 entries (tu | tv << 2), 8 bytes each,
     // one 128-byte bank row
     const uint32_t tabp = PRED ? tab + 128u * pre : tab + 8u * pre;
@@ -183,11 +188,21 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
             lastA = ta ? kx : lastA;
             pa += ta;
             pb += !ta;
-            const uint32_t nv = __ldg(adj + (ta ? pa : pb) + 1u);
-            x = ta ? xn : x;
-            xn = ta ? nv : xn;
-            y = ta ? y : yn;
-            yn = ta ? yn : nv;
+            if (LA2) {
+                const uint32_t nv = __ldg(adj + (ta ? pa : pb) + 2u);
+                x = ta ? xn : x;
+                xn = ta ? xnn : xn;
+                xnn = ta ? nv : xnn;
+                y = ta ? y : yn;
+                yn = ta ? yn : ynn;
+                ynn = ta ? ynn : nv;
+            } else {
+                const uint32_t nv = __ldg(adj + (ta ? pa : pb) + 1u);
+                x = ta ? xn : x;
+                xn = ta ? nv : xn;
+                y = ta ? y : yn;
+                yn = ta ? yn : nv;
+            }
         }
         // nibble 0 counts this dyad's intersection elements w > u (own-I)
         add_dyadic(c, pre, c.n4 & 15u);
@@ -198,6 +213,13 @@ __device__ __forceinline__ void merge_diag(const uint32_t *__restrict__ adj, uin
 // measured slower (C3 thread bin 1.49 ms at 54 registers, 1.03 ms capped at
 // 48; the shared table: 0.87 ms): the trip loop is issue-bound, and the
 // 64-bit variable shift + selects cost more issue slots than one LDS.64
+#ifndef TC_WARP_LA2
+#define TC_WARP_LA2 false
+#endif
+#ifndef TC_THREAD_LA2
+#define TC_THREAD_LA2 false
+#endif
+
 #ifndef TC_THREAD_REGTAB
 #define TC_THREAD_REGTAB 0
 #endif
@@ -479,7 +501,9 @@ k_census_thread(const BinItemT *__restrict__ items, const uint32_t *__restrict__
     block_finish_t(c, wsh, d_counts);
 #else
             warp_reserve(c, wsh[warp], e.t);
-            if (valid) merge_diag<false>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0, e.t, tab, c);
+            if (valid)
+                merge_diag<false, TC_THREAD_LA2>(adj, e.pa, 0, e.pb, 0, e.e | 3u, e.e & 3u, 0,
+                                                 e.t, tab, c);
         }
     }
     block_finish(c, wsh, d_counts);
@@ -662,7 +686,9 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
         const uint32_t span = e.d1 - e.d0, per = (span + 31) >> 5;
         const uint32_t d0 = e.d0 + min(span, lane * per), d1 = e.d0 + min(span, (lane + 1) * per);
         warp_reserve(c, wsh[warp], d1 - d0);
-        if (d0 < d1) merge_diag<true>(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1, tab, c);
+        if (d0 < d1)
+            merge_diag<true, TC_WARP_LA2>(adj, w.oa, w.a, w.ob, w.b, w.e | 3u, w.e & 3u, d0, d1,
+                                          tab, c);
     }
     block_finish(c, wsh, d_counts);
 }

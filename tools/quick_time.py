@@ -1,12 +1,21 @@
 """Quick per-phase timing of the CUDA path on one config (dev tool)."""
 import sys, time, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
 import torch
 import synth
 import paper_1603_02655_b200 as tcb
 
 name = sys.argv[1] if len(sys.argv) > 1 else "C3"
-a = synth.make_config(name)
+# arcs cached in /tmp for the duration of one gpurun call (A/B runs of many
+# library variants regenerate nothing)
+cache = "/tmp/tc_arcs_%s.npz" % name
+if os.path.exists(cache):
+    z = np.load(cache)
+    a = synth.Arcs(int(z["n"]), z["src"], z["dst"], {"config": name})
+else:
+    a = synth.make_config(name)
+    np.savez(cache, n=a.n, src=a.src, dst=a.dst)
 s = torch.from_numpy(a.src.view('int32')).cuda()
 d = torch.from_numpy(a.dst.view('int32')).cuda()
 for rep in range(4):
