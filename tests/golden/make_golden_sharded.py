@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--cache", default=None,
                     help="append finished ranges here (default: beside the output); "
                          "ranges cached in either file are skipped")
+    ap.add_argument("--note", default=None, help="free-text provenance note stored in the file")
     ap.add_argument("--no-write", action="store_true",
                     help="only fill the cache (another host writes the golden)")
     args = ap.parse_args()
@@ -88,6 +89,7 @@ def main():
                "oracle_cpu_seconds": round(cpu_s, 2),
                "sharding": {"ranges": len(ranges), "procs": args.procs, "kappa": sharded.KAPPA,
                             "cost": "d_u + d_v + kappa per canonical dyad (P:1693)"},
+               "note": args.note,
                "range_partials": [{"begin": b, "end": e, "partial": [str(x) for x in p]}
                                   for (b, e), p in zip(ranges, parts)],
                "written_by": "tests/golden/make_golden_sharded.py (oracle/ only)"}
