@@ -35,8 +35,6 @@
 // compaction.
 #include <stdio.h>
 
-#include <atomic>
-
 #include "radix_sort.cuh"
 #include "scan.cuh"
 
@@ -118,126 +116,6 @@ __device__ __forceinline__ bool chunk_head(const HeadChunk &c, int r, size_t L, 
     const uint64_t nf = __shfl_sync(0xffffffffu, c.k[r < kHcItems - 1 ? r + 1 : r], 0);
     if (lane == 31) nxt = r < kHcItems - 1 ? nf : c.after;
     return i < L && (i == 0 || (prev >> 2) != (k >> 2));
-}
-
-// ---------------------------------------------------------------------------
-// Row sort: the canonical keys are LSD-sorted by their row (min) bits only;
-// this kernel then sorts every row by (max, dir) -- the key's low word --
-// inside shared memory, replacing the LSD passes over the max bits.  Block b
-// owns the rows whose first key lies in [b T, (b+1) T) and loads them whole
-// (a segment of at most kRowCap keys): rows of <= 32 keys are insertion-
-// sorted by one thread each, longer rows by one warp each (bitonic network,
-// ascending comparators only, positions past the row end are +infinity).
-// A row that does not fit the segment sets *flag; the builder then re-sorts
-// all keys with the full LSD passes (exact either way).
-// ---------------------------------------------------------------------------
-constexpr int kRowTile = 4096;
-constexpr int kRowCap = 8192;             // keys per segment (64 KB of shared memory)
-constexpr int kRowThreads = 256;
-
-__device__ __forceinline__ bool row_start(const uint64_t *__restrict__ key, size_t L, size_t i) {
-    return i == 0 || i >= L || key_row(__ldg(key + i)) != key_row(__ldg(key + i - 1));
-}
-
-// first row start at or after p (p <= L), scanning at most kRowCap keys
-// (warp 0, all lanes); returns L + 1 if a row is longer than that
-__device__ __forceinline__ size_t next_row_start(const uint64_t *__restrict__ key, size_t L,
-                                                 size_t p) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (size_t base = p; base <= L && base < p + kRowCap; base += 32) {
-        const size_t i = base + lane;
-        const bool h = i <= L && row_start(key, L, i);
-        const uint32_t b = __ballot_sync(0xffffffffu, h);
-        if (b) return base + (__ffs(b) - 1);
-    }
-    return L + 1;
-}
-
-__global__ void __launch_bounds__(kRowThreads)
-k_row_sort(uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
-           unsigned long long *flag) {
-    extern __shared__ __align__(16) unsigned char row_smem[];
-    uint64_t *sk = reinterpret_cast<uint64_t *>(row_smem);
-    __shared__ size_t seg[2];
-    __shared__ uint32_t nlong;
-    __shared__ uint16_t starts[kRowCap + 1];   // row starts (segment-relative), then the end
-    __shared__ uint16_t longs[kRowTile];        // rows of more than 32 keys
-    const size_t L = m - *dropped;
-    const size_t t0 = (size_t)blockIdx.x * kRowTile;
-    if (t0 >= L) return;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (warp == 0) {
-        const size_t a = next_row_start(key, L, t0);
-        const size_t t1 = t0 + kRowTile < L ? t0 + kRowTile : L;
-        const size_t e = a <= L ? next_row_start(key, L, t1 > a ? t1 : a) : L + 1;
-        if (lane == 0) {
-            seg[0] = a;
-            seg[1] = e;
-            nlong = 0;
-        }
-    }
-    __syncthreads();
-    const size_t a = seg[0], e = seg[1];
-    if (a > L || e > L || e - a > (size_t)kRowCap) {   // a row longer than a segment
-        if (threadIdx.x == 0) atomicOr(flag, 1ull);
-        return;
-    }
-    const uint32_t len = (uint32_t)(e - a);
-    if (len == 0) return;
-    for (uint32_t i = threadIdx.x; i < len; i += kRowThreads) sk[i] = __ldg(key + a + i);
-    __syncthreads();
-    // row starts in order: each thread counts the starts in its chunk, a
-    // block scan places them
-    const uint32_t per = (len + kRowThreads - 1) / kRowThreads;
-    const uint32_t c0 = min(len, threadIdx.x * per), c1 = min(len, c0 + per);
-    uint32_t cnt = 0;
-    for (uint32_t i = c0; i < c1; i++)
-        cnt += (i == 0 || key_row(sk[i]) != key_row(sk[i - 1])) ? 1u : 0u;
-    uint32_t nr;
-    uint32_t o = block_exclusive_sum<uint32_t, kRowThreads>(cnt, &nr);
-    for (uint32_t i = c0; i < c1; i++)
-        if (i == 0 || key_row(sk[i]) != key_row(sk[i - 1])) starts[o++] = (uint16_t)i;
-    if (threadIdx.x == 0) starts[nr] = (uint16_t)len;
-    __syncthreads();
-    // short rows: one thread each (insertion sort on the low word)
-    for (uint32_t r = threadIdx.x; r < nr; r += kRowThreads) {
-        const uint32_t b0 = starts[r], b1 = starts[r + 1];
-        if (b1 - b0 > 32) {
-            longs[atomicAdd(&nlong, 1u)] = (uint16_t)r;
-            continue;
-        }
-        for (uint32_t i = b0 + 1; i < b1; i++) {
-            const uint64_t x = sk[i];
-            uint32_t j = i;
-            while (j > b0 && (uint32_t)sk[j - 1] > (uint32_t)x) {
-                sk[j] = sk[j - 1];
-                j--;
-            }
-            sk[j] = x;
-        }
-    }
-    __syncthreads();
-    // long rows: one warp each, bitonic network over the next power of two
-    for (uint32_t q = warp; q < nlong; q += kRowThreads / 32) {
-        const uint32_t r = longs[q], b0 = starts[r], n1 = starts[r + 1] - b0;
-        uint64_t *x = sk + b0;
-        uint32_t P = 1;
-        while (P < n1) P <<= 1;
-        for (uint32_t k = 2; k <= P; k <<= 1)
-            for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-                for (uint32_t i = lane; i < P; i += 32) {
-                    const uint32_t p = (j == (k >> 1)) ? (i ^ (k - 1)) : (i ^ j);
-                    if (p > i && p < n1 && (uint32_t)x[i] > (uint32_t)x[p]) {
-                        const uint64_t t = x[i];
-                        x[i] = x[p];
-                        x[p] = t;
-                    }
-                }
-                __syncwarp();
-            }
-    }
-    __syncthreads();
-    for (uint32_t i = threadIdx.x; i < len; i += kRowThreads) key[a + i] = sk[i];
 }
 
 // pass 1: per warp (512 keys), number of run heads
@@ -520,29 +398,15 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     // counts the dropped ones (no separate emit pass, no host round trip)
     int b = 1;
     while (b < 32 && (1ull << b) < n) b++;
-    // LSD passes over the row (min) bits, then the shared-memory row sort by
-    // (max, dir); if some row exceeds a row-sort segment (hub graphs), the
-    // keys are re-sorted with the full passes (max bits, then min bits)
     RadixPass passes[16];
-    int np = radix_passes_for(32, b, passes);
+    int np = radix_passes_for(2, b, passes);
+    np += radix_passes_for(32, b, passes + np);
     uint64_t *sorted = keys.p;
     if (m >= 2) {
         const ArcSource as{d_src, d_dst, n, scratch.p};
         if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
                                  &as)) != TC_OK)
             return st;
-        static std::atomic<uint64_t> attr_done{0};
-        int dev = 0;
-        TC_CUDA(cudaGetDevice(&dev));
-        if (!(attr_done.load() & (1ull << (dev & 63)))) {
-            TC_CUDA(cudaFuncSetAttribute(k_row_sort, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kRowCap * 8));
-            attr_done.fetch_or(1ull << (dev & 63));
-        }
-        k_row_sort<<<(unsigned)((m + kRowTile - 1) / kRowTile), kRowThreads, kRowCap * 8, s>>>(
-            sorted, m, scratch.p + 1, scratch.p + 2);
-        TC_CUDA(cudaGetLastError());
-        g->launches += 1;
     } else if (m == 1) {
         k_emit<<<1, 32, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
         g->launches++;
@@ -577,45 +441,31 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     uint32_t D = 0;
     DevBuf<uint32_t> total;
     if ((st = total.allocate(mem, 1)) != TC_OK) return st;
-    // 3. compaction (and the one mid-build host read: range check, dropped
-    // arcs, D -- which sizes the transposed sort and the adjacency -- and the
-    // row sort's long-row flag).  On the flag the keys are re-sorted with the
-    // full LSD passes (max bits, then min bits) and the compaction re-run.
-    unsigned long long h[8];
-    for (int attempt = 0;; attempt++) {
-        TC_CUDA(cudaMemsetAsync(total.p, 0, sizeof(uint32_t), s));
-        if (m) {
-            const size_t ntiles = (m + kHcTile - 1) / kHcTile;
-            DevBuf<uint32_t> wt;
-            if ((st = wt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
-            k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p);
-            TC_CUDA(cudaGetLastError());
-            st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
-                                          ArrayOutExcl<uint32_t>{wt.p}, total.p, s,
-                                          &g->launches);
-            if (st != TC_OK) return st;
-            k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p,
-                                                                 du, de, spare, dpb, up_start.p);
-            TC_CUDA(cudaGetLastError());
-            g->launches += 2;
-        }
-        // rows after the last canonical row have no upper entries
-        k_fill_tail_up<<<grid_for(n + 1, 256), 256, 0, s>>>(up_start.p, sorted, m,
-                                                            scratch.p + 1, n, total.p);
+    TC_CUDA(cudaMemsetAsync(total.p, 0, sizeof(uint32_t), s));
+    if (m) {
+        const size_t ntiles = (m + kHcTile - 1) / kHcTile;
+        DevBuf<uint32_t> wt;
+        if ((st = wt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
+        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p);
         TC_CUDA(cudaGetLastError());
-        TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-        TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-        TC_CUDA(cudaStreamSynchronize(s));
-        if (!h[2] || attempt > 0 || h[0] != ~0ull) break;
-        RadixPass full[16];
-        int nf = radix_passes_for(2, b, full);
-        nf += radix_passes_for(32, b, full + nf);
-        uint64_t *re = sorted;
-        if ((st = radix_sort_u64(mem, sorted, spare, m, full, nf, s, &g->launches, &re)) != TC_OK)
-            return st;
-        spare = re == keys.p ? tmp.p : keys.p;
-        sorted = re;
+        st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
+                                      ArrayOutExcl<uint32_t>{wt.p}, total.p, s, &g->launches);
+        if (st != TC_OK) return st;
+        k_head_write<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p, du,
+                                                             de, spare, dpb, up_start.p);
+        TC_CUDA(cudaGetLastError());
+        g->launches += 2;
     }
+    // rows after the last canonical row have no upper entries
+    k_fill_tail_up<<<grid_for(n + 1, 256), 256, 0, s>>>(up_start.p, sorted, m, scratch.p + 1, n,
+                                                        total.p);
+    TC_CUDA(cudaGetLastError());
+    // the one mid-build host read: range check, dropped arcs, D (sizes the
+    // transposed sort and the adjacency)
+    unsigned long long h[8];
+    TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaStreamSynchronize(s));
     if (h[0] != ~0ull) {
         set_error("arc %llu has an endpoint >= n (n = %llu)", h[0], (unsigned long long)n);
         return TC_E_RANGE;

@@ -77,40 +77,6 @@ __device__ __forceinline__ uint32_t sparse_mode(const PlanIn &P, uint64_t i, uin
     return a < b ? 1u : 2u;
 }
 
-// the merge lengths t of the warp's 512 dyads (iteration k holds dyad base +
-// 32 k + lane) and their stable ranks among the warp's dyads of equal digit
-// (one ballot per digit bit groups the lanes holding the same digit)
-template <bool FULL>
-__device__ __forceinline__ void plan_rank(const PlanIn &P, uint64_t N, uint64_t base, uint32_t *wc,
-                                          uint32_t (&cst)[kPlanItems],
-                                          uint32_t (&rank)[kPlanItems]) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
-#pragma unroll
-    for (int k = 0; k < kPlanItems; k++) {
-        const uint64_t i = base + k * 32 + lane;
-        cst[k] = (FULL || i < N) ? __ldg(P.dt + i) : 0u;
-    }
-#pragma unroll
-    for (int k = 0; k < kPlanItems; k++) {
-        const uint64_t i = base + k * 32 + lane;
-        const bool valid = FULL || i < N;
-        const uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
-        uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bit = 0; bit < 8; bit++) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-            peers &= ((d >> bit) & 1u) ? b : ~b;
-        }
-        uint32_t r = 0;
-        if (valid) r = wc[d] + __popc(peers & lt);
-        __syncwarp();
-        if (valid && (peers & lt) == 0) wc[d] += __popc(peers);
-        __syncwarp();
-        rank[k] = r;
-    }
-}
-
 template <bool SPARSE>
 __global__ void __launch_bounds__(kPlanThreads)
 k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
@@ -121,14 +87,30 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kPlanWarps * kDigits; i += kPlanThreads) (&wc[0][0])[i] = 0;
     __syncthreads();
+    const uint32_t lt = (1u << lane) - 1u;
     const uint64_t tile0 = (uint64_t)blockIdx.x * kPlanTile;
     const uint32_t wbase = warp * 32 * kPlanItems;
     uint32_t cst[kPlanItems], rank[kPlanItems];
-    // every tile but the last is full: no per-dyad bounds checks there
-    if (tile0 + kPlanTile <= N)
-        plan_rank<true>(P, N, tile0 + wbase, wc[warp], cst, rank);
-    else
-        plan_rank<false>(P, N, tile0 + wbase, wc[warp], cst, rank);
+#pragma unroll
+    for (int k = 0; k < kPlanItems; k++) {
+        uint64_t i = tile0 + wbase + k * 32 + lane;
+        bool valid = i < N;
+        cst[k] = valid ? __ldg(P.dt + i) : 0u;
+        uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
+        // lanes holding the same digit: one ballot per digit bit
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bit = 0; bit < 8; bit++) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+            peers &= ((d >> bit) & 1u) ? b : ~b;
+        }
+        uint32_t r = 0;
+        if (valid) r = wc[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
+        rank[k] = r;
+    }
     __syncthreads();
     uint32_t all;   // thread-bin dyads of the tile
     {   // thread d owns digit d: tile-local offsets (digit-major, then warp)
