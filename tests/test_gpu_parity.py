@@ -325,3 +325,46 @@ def test_skewed_pair_path_vs_oracle(tcb, seed):
             assert tcb.tc_census_range(g, b, e) == og.census_range(b, e)
     finally:
         g.close()
+
+
+def test_concurrent_census_on_shared_graph(tcb):
+    # include/triadcensus.h: a graph may be shared by concurrent census calls
+    # on different streams (host threads); each call publishes its own launch
+    # count / profile under the graph's mutex
+    import threading
+    import torch
+    a = synth.make_config("C2")
+    g = tcb.tc_graph_create(a.n, a.src, a.dst)
+    g.profile(True)
+    want = g.census()
+    og = oracle.Graph(a.n, a.src, a.dst)
+    D = og.stats()["dyads"]
+    out, errs = {}, []
+
+    def work(t):
+        try:
+            torch.cuda.set_device(0)
+            s = torch.cuda.Stream()
+            for rep in range(5):
+                if t % 2:
+                    out[(t, rep)] = g.census(stream=s)
+                else:
+                    b, e = (t * 997) % D, min(D, (t * 997) % D + 5000)
+                    out[(t, rep)] = (b, e, tcb.tc_census_range(g, b, e, stream=s))
+        except Exception as ex:   # pragma: no cover - reported below
+            errs.append(ex)
+
+    th = [threading.Thread(target=work, args=(t,)) for t in range(6)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for (t, rep), v in out.items():
+        if t % 2:
+            assert v == want
+        else:
+            b, e, part = v
+            assert part == og.census_range(b, e)
+    assert g.launches() > 0 and g.profile_get()["census_ms"] > 0
+    g.close()
