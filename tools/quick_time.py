@@ -10,15 +10,22 @@ name = sys.argv[1] if len(sys.argv) > 1 else "C3"
 # arcs cached in /tmp for the duration of one gpurun call (A/B runs of many
 # library variants regenerate nothing)
 cache = "/tmp/tc_arcs_%s.npz" % name
-if os.path.exists(cache):
+from synth.device import DEVICE_CONFIGS, make_device_config
+if name in DEVICE_CONFIGS:
+    n_, s_, d_, _ = make_device_config(name, torch.device("cuda", 0))
+    a = synth.Arcs(n_, None, None, {"config": name})
+elif os.path.exists(cache):
     z = np.load(cache)
     a = synth.Arcs(int(z["n"]), z["src"], z["dst"], {"config": name})
 else:
     a = synth.make_config(name)
     np.savez(cache, n=a.n, src=a.src, dst=a.dst)
-s = torch.from_numpy(a.src.view('int32')).cuda()
-d = torch.from_numpy(a.dst.view('int32')).cuda()
-for rep in range(4):
+if a.src is None:
+    s, d = s_, d_
+else:
+    s = torch.from_numpy(a.src.view('int32')).cuda()
+    d = torch.from_numpy(a.dst.view('int32')).cuda()
+for rep in range(2 if name in DEVICE_CONFIGS else 4):
     torch.cuda.synchronize(); t0 = time.perf_counter()
     g = tcb.tc_graph_create(a.n, s, d, use_torch_allocator=os.environ.get("TC_TORCH_ALLOC", "1") == "1")
     torch.cuda.synchronize(); t1 = time.perf_counter()
