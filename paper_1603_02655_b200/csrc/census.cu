@@ -551,37 +551,9 @@ __device__ __forceinline__ uint32_t lower_id(const uint32_t *__restrict__ L, uin
     return lo;
 }
 
-// lower_id through a splitter sample of L in shared memory: samp[k] =
-// id(L[k len / 256]) (k < 256, ascending).  The samples below x (a binary
-// search in shared memory) bound the answer to one window of ~len / 256
-// entries, searched in global memory: half the dependent L2 probes of a
-// plain binary search over L on long lists.
-#ifndef TC_SP_SAMPLE
-#define TC_SP_SAMPLE 1
-#endif
-constexpr uint32_t kSpSamples = 256;
-__device__ __forceinline__ uint32_t lower_id_sampled(const uint32_t *__restrict__ L, uint32_t len,
-                                                     uint32_t x, const uint32_t *samp) {
-    uint32_t lo = 0, hi = kSpSamples;   // number of samples with id < x
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (samp[mid] < x) lo = mid + 1;
-        else hi = mid;
-    }
-    if (lo == 0) return 0;              // id(L[0]) >= x
-    uint32_t a = (uint32_t)(((uint64_t)(lo - 1) * len) / kSpSamples) + 1;
-    uint32_t b = lo < kSpSamples ? (uint32_t)(((uint64_t)lo * len) / kSpSamples) : len;
-    while (a < b) {                     // answer in [a, b]
-        const uint32_t mid = (a + b) >> 1;
-        if ((__ldg(L + mid) >> 2) < x) a = mid + 1;
-        else b = mid;
-    }
-    return a;
-}
-
-__device__ __forceinline__ uint32_t tag_in_s(const uint32_t *__restrict__ L, uint32_t len,
-                                             uint32_t x, const uint32_t *samp) {
-    const uint32_t p = samp ? lower_id_sampled(L, len, x, samp) : lower_id(L, len, x);
+__device__ __forceinline__ uint32_t tag_in(const uint32_t *__restrict__ L, uint32_t len,
+                                           uint32_t x) {
+    const uint32_t p = lower_id(L, len, x);
     if (p < len) {
         const uint32_t e = __ldg(L + p);
         if ((e >> 2) == x) return e & 3u;
@@ -626,32 +598,16 @@ __device__ __forceinline__ void sp_drain(sp_t *sp, unsigned long long *wsh) {
 
 __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__restrict__ P,
                             const WarpDyad &w, uint32_t mode, uint32_t d0, uint32_t d1,
-                            sp_t *sp, uint32_t *samp_s) {
+                            sp_t *sp) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t v = w.e >> 2, pre = w.e & 3u;
     const uint32_t minus1 = ~0u;
     uint32_t own = 0, o012 = 0, o102 = 0;
-    // splitter sample of the searched (long) list, when it pays: a long list
-    // and enough short-list entries in this item to amortise 256 loads
-    const uint32_t *samp = nullptr;
-#if TC_SP_SAMPLE
-    {
-        const uint32_t *Ls = mode == 1u ? adj + w.ob : adj + w.oa;
-        const uint32_t ls = mode == 1u ? w.b : w.a;
-        if (ls >= 4 * kSpSamples && d1 - d0 >= 64) {
-#pragma unroll
-            for (uint32_t k = lane; k < kSpSamples; k += 32)
-                samp_s[k] = __ldg(Ls + (uint32_t)(((uint64_t)k * ls) / kSpSamples)) >> 2;
-            __syncwarp();
-            samp = samp_s;
-        }
-    }
-#endif
     if (mode == 1u) {
         for (uint32_t j = d0 + lane; j < d1; j += 32) {
             const uint32_t x = __ldg(adj + w.oa + j), id = x >> 2, tu = x & 3u;
             if (id == v) continue;
-            const uint32_t tv = tag_in_s(adj + w.ob, w.b, id, samp);
+            const uint32_t tv = tag_in(adj + w.ob, w.b, id);
             if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
             if (tv) {
                 own++;
@@ -672,7 +628,7 @@ __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__
     } else {
         for (uint32_t j = d0 + lane; j < d1; j += 32) {
             const uint32_t y = __ldg(adj + w.ob + j), id = y >> 2, tv = y & 3u;
-            const uint32_t tu = tag_in_s(adj + w.oa, w.a, id, samp);
+            const uint32_t tu = tag_in(adj + w.oa, w.a, id);
             if (!tu) {
                 sp_add(sp, c_triad_table[pre | tv << 4], 1u);
             } else {
@@ -694,7 +650,6 @@ __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__
                 if (cnt[t]) sp_add(sp, c_triad_table[pre | t << 2], cnt[t]);
         }
     }
-    __syncwarp();   // samp_s is reused by the warp's next item
     // own I -> the dyad's dyadic class; owed dyadic triads by tv
     own = __reduce_add_sync(0xffffffffu, own);
     o012 = __reduce_add_sync(0xffffffffu, o012);
@@ -720,7 +675,6 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
     acc_init(c);
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ sp_t spw[kWarps][16];   // skewed-pair class counts, per warp (wrapping)
-    __shared__ uint32_t samp_s[kWarps][kSpSamples];   // skewed pairs: long-list splitters
     if (lane < 16) spw[warp][lane] = 0;
     __syncwarp();
     const uint64_t count = *L.w_count;
@@ -728,7 +682,7 @@ k_census_warp(const BinLists L, const uint32_t *__restrict__ off, const uint32_t
         const BinItemW e = L.w[it];
         const WarpDyad w = warp_dyad(L, off, ups, e.k);
         if (e.pad) {   // warp-uniform
-            sparse_item(adj, L.tagpre, w, e.pad, e.d0, e.d1, spw[warp], samp_s[warp]);
+            sparse_item(adj, L.tagpre, w, e.pad, e.d0, e.d1, spw[warp]);
             sp_drain(spw[warp], wsh[warp]);
             continue;
         }
