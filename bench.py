@@ -312,7 +312,11 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def one_step(src, dst, profile=False):
-        g = tcb.tc_graph_create(a.n, src, dst, device=local, stream=stream)
+        # the library's own stream-ordered pool (the ABI's default allocator)
+        # rather than torch's caching allocator through the Python hook: no
+        # Python callback per device allocation on the build's critical path
+        g = tcb.tc_graph_create(a.n, src, dst, device=local, stream=stream,
+                                use_torch_allocator=False)
         launches = g.launches()
         if profile:
             g.profile(True)
