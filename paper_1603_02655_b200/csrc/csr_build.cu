@@ -10,16 +10,21 @@
 //                an endpoint >= n -> all-ones sentinel keys that sort last
 //                (strict digraph); computed by the first radix
 //                pass straight from the arc list, which also counts them.
-//   2. sort      LSD radix sort (radix_sort.cu) on the max bits, then the
-//                min bits: canonical pairs in the algorithm's own dyad order
-//                (u ascending, v ascending).
+//   2. sort      LSD radix sort (radix_sort.cu) on the min (row) bits, then
+//                a row sort (k_row_sort: shuffle ranking for rows <= 32 keys,
+//                a shared-memory bitonic network up to kRowMed) by the max
+//                bits: canonical pairs in the algorithm's own dyad order (u
+//                ascending, v ascending).  Graphs with a row of
+//                more than kRowMed keys take the full LSD (max bits, then min
+//                bits) instead.
 //   3. compact   a ballot/popc compaction keeps the first key of each (min,
 //                max) run with the OR of the run's direction bits (dedup +
 //                mutual merge): the canonical dyad list dyad_u / dyad_e (the
 //                upper halves of the rows), the transposed keys (max<<32 |
 //                dyad index) and the lower entries (min<<2 | swapped tag).
 //   4. sort      stable LSD sort of the D transposed keys on the row bits
-//                only (they arrive sorted by min, so each row ends up sorted).
+//                only (they arrive sorted by min, so each row ends up sorted);
+//                D is read on the device (no host round trip).
 //   5. assemble  row u = lower part (w < u) then upper part (w > u), both
 //                already sorted, then one sentinel 0xffffffff (greater than
 //                any real entry) so the census merge runs off a row end
@@ -118,6 +123,210 @@ __device__ __forceinline__ bool chunk_head(const HeadChunk &c, int r, size_t L, 
     return i < L && (i == 0 || (prev >> 2) != (k >> 2));
 }
 
+// ---------------------------------------------------------------------------
+// Row sort (step 2, round 2): the LSD passes run over the min (row) bits only,
+// so the keys leave the sort grouped by row (rows in ascending order) but
+// unordered inside a row; each row is then ordered by its low word (max << 2 |
+// dir) in place, instead of ceil(b / 8) more LSD passes over all m keys.  Rows
+// are independent, so they are sorted by length class:
+//   k_row_bounds    start / end of every row (the keys at row changes)
+//   k_row_classify  per vertex: length class -> the class's work list
+//   k_row_sort_net  rows of <= 8 / 16 / 32 keys: one THREAD per row, the
+//                   row's low words in registers through a bitonic network
+//   k_row_sort_warp rows of 33..kRowMed keys: one warp per row, a bitonic
+//                   network over the low words in shared memory
+// Rows of more than kRowMed keys are only counted: the host then reruns the
+// full LSD (max bits, then min bits) instead (hub graphs).
+// Keys equal in (row, max) are duplicates or the two arcs of a mutual pair;
+// the compaction merges them in any order.
+// ---------------------------------------------------------------------------
+constexpr int kRowMed = 1024;
+constexpr int kRowClasses = 5;   // <= 8, <= 16, <= 32, <= kRowMed, larger
+
+__global__ void k_row_bounds(const uint64_t *__restrict__ X, size_t m,
+                             const unsigned long long *__restrict__ dropped,
+                             uint32_t *__restrict__ rstart, uint32_t *__restrict__ rend) {
+    const size_t L = m - *dropped;
+    const uint32_t lane = threadIdx.x & 31;
+    const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;   // one key per thread
+    if (p - lane >= L) return;   // warp-uniform
+    const uint32_t r = p < L ? (uint32_t)(__ldg(X + p) >> 32) : ~0u;
+    uint32_t prv = __shfl_up_sync(0xffffffffu, r, 1);
+    uint32_t nxt = __shfl_down_sync(0xffffffffu, r, 1);
+    if (lane == 0) prv = p ? (uint32_t)(__ldg(X + p - 1) >> 32) : ~r;
+    if (lane == 31) nxt = p + 1 < L ? (uint32_t)(__ldg(X + p + 1) >> 32) : ~r;
+    if (p < L) {
+        if (prv != r) rstart[r] = (uint32_t)p;
+        if (nxt != r) rend[r] = (uint32_t)(p + 1);
+    }
+}
+
+__device__ __forceinline__ int row_class(uint32_t len) {
+    return len <= 1 ? -1 : len <= 8 ? 0 : len <= 16 ? 1 : len <= 32 ? 2
+         : len <= (uint32_t)kRowMed ? 3 : 4;
+}
+
+// lists: kRowClasses arrays of n entries each; cnt[c] = entries of class c.
+// Each block takes one contiguous range of vertices: it counts its classes,
+// reserves them with one atomic per class (no contention on the counters),
+// then writes its entries (vertex order inside the block's share).
+constexpr int kRcThreads = 256;
+__global__ void __launch_bounds__(kRcThreads)
+k_row_classify(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ rend,
+               uint64_t n, uint32_t *__restrict__ lists, unsigned long long *__restrict__ cnt) {
+    __shared__ uint32_t wcnt[kRcThreads / 32][kRowClasses];
+    __shared__ unsigned long long base[kRowClasses];
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint64_t per = (n + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = (uint64_t)blockIdx.x * per, u1 = min(n, u0 + per);
+    if (threadIdx.x < kRcThreads / 32 * kRowClasses) (&wcnt[0][0])[threadIdx.x] = 0;
+    __syncthreads();
+    // pass 1: per-warp class counts over the block's range
+    uint32_t c_loc[kRowClasses] = {0, 0, 0, 0, 0};
+    for (uint64_t u = u0 + threadIdx.x; u < u1; u += kRcThreads) {
+        const int c = row_class(__ldg(rend + u) - __ldg(rstart + u));
+#pragma unroll
+        for (int k = 0; k < kRowClasses; k++) c_loc[k] += c == k;
+    }
+#pragma unroll
+    for (int k = 0; k < kRowClasses; k++) {
+        const uint32_t t = __reduce_add_sync(0xffffffffu, c_loc[k]);
+        if (lane == 0) wcnt[warp][k] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < kRowClasses) {
+        uint32_t t = 0;
+        for (int w = 0; w < kRcThreads / 32; w++) t += wcnt[w][threadIdx.x];
+        base[threadIdx.x] = t ? atomicAdd(&cnt[threadIdx.x], (unsigned long long)t) : 0ull;
+    }
+    __syncthreads();
+    // pass 2: block-ordered write positions (running per-class offsets)
+    for (uint64_t u00 = u0; u00 < u1; u00 += kRcThreads) {
+        const uint64_t u = u00 + threadIdx.x;
+        const int c = u < u1 ? row_class(__ldg(rend + u) - __ldg(rstart + u)) : -1;
+        uint32_t mine = 0;
+#pragma unroll
+        for (int k = 0; k < kRowClasses; k++) {
+            const uint32_t bal = __ballot_sync(0xffffffffu, c == k);
+            if (lane == 0) wcnt[warp][k] = __popc(bal);
+            if (c == k) mine = __popc(bal & ((1u << lane) - 1u));
+        }
+        __syncthreads();
+        if (c >= 0) {
+            uint32_t off = 0;
+            for (int w = 0; w < (int)warp; w++) off += wcnt[w][c];
+            lists[(size_t)c * n + base[c] + off + mine] = (uint32_t)u;
+        }
+        __syncthreads();
+        if (threadIdx.x < kRowClasses) {
+            uint32_t t = 0;
+            for (int w = 0; w < kRcThreads / 32; w++) t += wcnt[w][threadIdx.x];
+            base[threadIdx.x] += t;
+        }
+        __syncthreads();
+    }
+}
+
+// one thread per row of <= P keys: bitonic network over the low words
+template <int P>
+__global__ void __launch_bounds__(128)
+k_row_sort_net(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
+               const uint32_t *__restrict__ rend, const uint32_t *__restrict__ list,
+               const unsigned long long *__restrict__ cnt) {
+    const uint64_t nr = *cnt;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t u = __ldg(list + i);
+        const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
+        uint32_t v[P];
+#pragma unroll
+        for (int j = 0; j < P; j++) v[j] = j < (int)len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
+#pragma unroll
+        for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+            for (int h = k >> 1; h > 0; h >>= 1) {
+#pragma unroll
+                for (int j = 0; j < P; j++) {
+                    const int x = j ^ h;
+                    if (x > j) {
+                        const uint32_t a = v[j], b = v[x];
+                        const bool up = (j & k) == 0;
+                        v[j] = up ? min(a, b) : max(a, b);
+                        v[x] = up ? max(a, b) : min(a, b);
+                    }
+                }
+            }
+        }
+        const uint64_t hi = (uint64_t)u << 32;
+#pragma unroll
+        for (int j = 0; j < P; j++)
+            if (j < (int)len) X[s0 + j] = hi | v[j];
+    }
+}
+
+// one warp per row of 33..kRowMed keys: bitonic network in shared memory
+constexpr int kRswThreads = 256;
+__global__ void __launch_bounds__(kRswThreads)
+k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
+                const uint32_t *__restrict__ rend, const uint32_t *__restrict__ list,
+                const unsigned long long *__restrict__ cnt) {
+    __shared__ uint32_t buf[kRswThreads / 32][kRowMed];
+    const uint64_t nr = *cnt;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t *b = buf[warp];
+    const size_t nw = ((size_t)gridDim.x * kRswThreads) >> 5;
+    for (size_t i = ((size_t)blockIdx.x * kRswThreads + threadIdx.x) >> 5; i < nr; i += nw) {
+        const uint32_t u = __ldg(list + i);
+        const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
+        const uint64_t hi = (uint64_t)u << 32;
+        if (len <= 64) {   // two elements per lane, network across lanes by shuffles
+            uint32_t e0 = lane < len ? (uint32_t)__ldg(X + s0 + lane) : ~0u;
+            uint32_t e1 = lane + 32 < len ? (uint32_t)__ldg(X + s0 + 32 + lane) : ~0u;
+#pragma unroll
+            for (uint32_t k = 2; k <= 64; k <<= 1) {
+#pragma unroll
+                for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+                    if (h == 32) {   // partner in the same lane: (lane, lane + 32), k = 64: ascending
+                        const uint32_t lo = min(e0, e1), hv = max(e0, e1);
+                        e0 = lo;
+                        e1 = hv;
+                    } else {
+                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, h);
+                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, e1, h);
+                        // element index e = lane (+ 32); keep the min iff ascending == lower
+                        const bool lower = (lane & h) == 0;
+                        const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+                        e0 = (up0 == lower) ? min(e0, o0) : max(e0, o0);
+                        e1 = (up1 == lower) ? min(e1, o1) : max(e1, o1);
+                    }
+                }
+            }
+            if (lane < len) X[s0 + lane] = hi | e0;
+            if (lane + 32 < len) X[s0 + 32 + lane] = hi | e1;
+            continue;
+        }
+        uint32_t P = 128;
+        while (P < len) P <<= 1;
+        for (uint32_t j = lane; j < P; j += 32) b[j] = j < len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
+        __syncwarp();
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+            for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+                // P / 2 compare-exchanges per step, one pair (j, j ^ h), j with bit h clear
+                for (uint32_t q = lane; q < P / 2; q += 32) {
+                    const uint32_t j = ((q & ~(h - 1)) << 1) | (q & (h - 1)), x = j | h;
+                    const uint32_t va = b[j], vb = b[x];
+                    const bool up = (j & k) == 0;
+                    b[j] = up ? min(va, vb) : max(va, vb);
+                    b[x] = up ? max(va, vb) : min(va, vb);
+                }
+                __syncwarp();
+            }
+        }
+        for (uint32_t j = lane; j < len; j += 32) X[s0 + j] = hi | b[j];
+        __syncwarp();
+    }
+}
+
 // pass 1: per warp (512 keys), number of run heads
 __global__ void __launch_bounds__(kHcThreads)
 k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
@@ -200,9 +409,10 @@ k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
 // the random L2 round trips overlap instead of serialising behind the
 // (possibly aliasing) ul[k] stores of the previous key.
 constexpr int kWlBatch = 4;
-__global__ void k_write_lower(const uint64_t *__restrict__ tk, size_t D,
+__global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *__restrict__ dD,
                               const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
                               uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start) {
+    const size_t D = *dD;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < D;
          i0 += kWlBatch * stride) {
@@ -252,8 +462,10 @@ __global__ void k_fill_tail_up(uint32_t *start, const uint64_t *__restrict__ key
 
 // start[x] = val for x in (row of the last key, n]: the rows after the last
 // one of a row-sorted key array (read on the device: no host round trip)
-__global__ void k_fill_tail_last(uint32_t *start, const uint64_t *__restrict__ key, uint64_t L,
-                                 uint64_t n, uint32_t val) {
+__global__ void k_fill_tail_last(uint32_t *start, const uint64_t *__restrict__ key,
+                                 const uint32_t *__restrict__ dL, uint64_t n) {
+    const uint32_t val = *dL;
+    const uint64_t L = val;
     const uint64_t from = L ? (uint64_t)key_row(key[L - 1]) + 1 : 0;
     for (uint64_t x = from + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x <= n;
          x += (uint64_t)gridDim.x * blockDim.x)
@@ -306,9 +518,10 @@ __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
 __global__ void k_write_upper(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
                               const uint32_t *__restrict__ lo_start,
                               const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
-                              const uint32_t *__restrict__ dpb, uint64_t D,
+                              const uint32_t *__restrict__ dpb, const uint32_t *__restrict__ dD,
                               uint32_t *__restrict__ adj, uint32_t *__restrict__ dc,
                               uint32_t *__restrict__ dt, unsigned long long *out) {
+    const uint64_t D = *dD;
     unsigned long long m = 0, mu = 0;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     // kWlBatch dyads per thread, all loads (the random off[v], off[v+1] among
@@ -399,14 +612,55 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     int b = 1;
     while (b < 32 && (1ull << b) < n) b++;
     RadixPass passes[16];
-    int np = radix_passes_for(2, b, passes);
-    np += radix_passes_for(32, b, passes + np);
     uint64_t *sorted = keys.p;
+    uint64_t dropped_h = 0;   // loops + out-of-range arcs (host copy, m >= 2)
     if (m >= 2) {
         const ArcSource as{d_src, d_dst, n, scratch.p};
+        // LSD over the row (min) bits only, then the row sort (above)
+        int np = radix_passes_for(32, b, passes);
         if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
                                  &as)) != TC_OK)
             return st;
+        // row sort, in place in `sorted`
+        DevBuf<uint32_t> rb, lists;
+        DevBuf<unsigned long long> rc;
+        if ((st = rb.allocate(mem, 2 * (n + 1))) != TC_OK) return st;
+        if ((st = lists.allocate(mem, (size_t)kRowClasses * n)) != TC_OK) return st;
+        if ((st = rc.allocate(mem, kRowClasses)) != TC_OK) return st;
+        uint32_t *rstart = rb.p, *rend = rb.p + n + 1;
+        TC_CUDA(cudaMemsetAsync(rb.p, 0, 2 * (n + 1) * sizeof(uint32_t), s));
+        TC_CUDA(cudaMemsetAsync(rc.p, 0, kRowClasses * sizeof(unsigned long long), s));
+        k_row_bounds<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(sorted, m, scratch.p + 1, rstart,
+                                                                 rend);
+        k_row_classify<<<grid_for(n, kRcThreads, 148 * 8), kRcThreads, 0, s>>>(rstart, rend, n,
+                                                                         lists.p, rc.p);
+        const unsigned gnet = grid_for(n, 128, 148 * 64);
+        k_row_sort_net<8><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p, rc.p);
+        k_row_sort_net<16><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p + n, rc.p + 1);
+        k_row_sort_net<32><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p + 2 * n, rc.p + 2);
+        k_row_sort_warp<<<148 * 4, kRswThreads, 0, s>>>(sorted, rstart, rend, lists.p + 3 * n,
+                                                        rc.p + 3);
+        TC_CUDA(cudaGetLastError());
+        g->launches += 6;
+        // host read: range check, and whether a row exceeded kRowMed keys
+        unsigned long long h0[2], rch[kRowClasses];
+        TC_CUDA(cudaMemcpyAsync(h0, scratch.p, sizeof(h0), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaMemcpyAsync(rch, rc.p, sizeof(rch), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        if (h0[0] != ~0ull) {
+            set_error("arc %llu has an endpoint >= n (n = %llu)", h0[0], (unsigned long long)n);
+            return TC_E_RANGE;
+        }
+        dropped_h = h0[1];
+        if (rch[kRowClasses - 1]) {   // hub rows: the full LSD, max bits then min bits, from the arcs again
+            unsigned long long init2[2] = {~0ull, 0};
+            TC_CUDA(cudaMemcpyAsync(scratch.p, init2, sizeof(init2), cudaMemcpyHostToDevice, s));
+            np = radix_passes_for(2, b, passes);
+            np += radix_passes_for(32, b, passes + np);
+            if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
+                                     &as)) != TC_OK)
+                return st;
+        }
     } else if (m == 1) {
         k_emit<<<1, 32, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
         g->launches++;
@@ -460,21 +714,27 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     k_fill_tail_up<<<grid_for(n + 1, 256), 256, 0, s>>>(up_start.p, sorted, m, scratch.p + 1, n,
                                                         total.p);
     TC_CUDA(cudaGetLastError());
-    // the one mid-build host read: range check, dropped arcs, D (sizes the
-    // transposed sort and the adjacency)
+    // D stays on the device (total.p): the transposed sort and the assembly
+    // kernels read it there and are sized by the host-side bound Dub (the
+    // canonical key count L, known from the row sort's host read), so the
+    // build has one host round trip.  Graphs whose bound could overflow the
+    // 32-bit offsets (2 Dub + n >= 2^32), and m < 2, read D exactly here.
     unsigned long long h[8];
-    TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-    TC_CUDA(cudaStreamSynchronize(s));
-    if (h[0] != ~0ull) {
-        set_error("arc %llu has an endpoint >= n (n = %llu)", h[0], (unsigned long long)n);
-        return TC_E_RANGE;
-    }
-    const uint64_t loops = h[1];
-    if (2ull * D + n + 8 >= (1ull << 32)) {
-        set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
-                  (unsigned long long)(2ull * D + n));
-        return TC_E_INVALID;
+    uint64_t Dub = m >= 2 ? m - dropped_h : 0;
+    if (m < 2 || 2ull * Dub + n + 8 >= (1ull << 32)) {
+        TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaStreamSynchronize(s));
+        if (h[0] != ~0ull) {
+            set_error("arc %llu has an endpoint >= n (n = %llu)", h[0], (unsigned long long)n);
+            return TC_E_RANGE;
+        }
+        if (2ull * D + n + 8 >= (1ull << 32)) {
+            set_error("2D + n = %llu exceeds the 32-bit CSR offset range",
+                      (unsigned long long)(2ull * D + n));
+            return TC_E_INVALID;
+        }
+        Dub = D;
     }
 
     // 4. lower halves: stable sort of the transposed keys on the row bits
@@ -482,35 +742,38 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     RadixPass rpasses[8];
     const int nrp = radix_passes_for(32, b, rpasses);
     uint64_t *tother = spare == keys.p ? tmp.p : keys.p;
-    if ((st = radix_sort_u64(mem, spare, tother, D, rpasses, nrp, s, &g->launches, &tsorted)) !=
-        TC_OK)
+    if ((st = radix_sort_u64(mem, spare, tother, Dub, rpasses, nrp, s, &g->launches, &tsorted,
+                             nullptr, total.p)) != TC_OK)
         return st;
     // 5. assemble the symmetric rows: lower entries (+ lo_start, dyad_pb),
     // then offsets, sentinels and vertex stats, then upper entries
-    const uint64_t nnz = 2ull * D;
-    uint32_t *adj = (uint32_t *)mem.alloc((nnz + n + 8) * sizeof(uint32_t));
-    g->adj = adj; g->adj_n = nnz + n + 8;
+    uint32_t *adj = (uint32_t *)mem.alloc((2ull * Dub + n + 8) * sizeof(uint32_t));
+    g->adj = adj;
     if (!adj) {
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
     }
-    if (D) {
-        k_write_lower<<<grid_for(D, 256), 256, 0, s>>>(tsorted, D, up_start.p, adj, dpb,
-                                                       lo_start.p);
+    if (Dub) {
+        k_write_lower<<<grid_for(Dub, 256), 256, 0, s>>>(tsorted, total.p, up_start.p, adj, dpb,
+                                                         lo_start.p);
         g->launches += 1;
     }
-    k_fill_tail_last<<<grid_for(n + 1, 256), 256, 0, s>>>(lo_start.p, tsorted, D, n, D);
+    k_fill_tail_last<<<grid_for(n + 1, 256), 256, 0, s>>>(lo_start.p, tsorted, total.p, n);
     k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj,
                                                    scratch.p + 4);
     g->launches += 2;
-    if (D) {
-        k_write_upper<<<grid_for(D, 256), 256, 0, s>>>(off, ups, lo_start.p, du, de, dpb, D, adj,
-                                                       dc, dt, scratch.p + 4);
+    if (Dub) {
+        k_write_upper<<<grid_for(Dub, 256), 256, 0, s>>>(off, ups, lo_start.p, du, de, dpb,
+                                                         total.p, adj, dc, dt, scratch.p + 4);
         g->launches += 1;
     }
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
+    TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
+    const uint64_t loops = h[1];
+    const uint64_t nnz = 2ull * D;
+    g->adj_n = nnz + n + 8;
     // 7. tag prefix counts for the skewed-pair path (hub graphs only)
     if (h[5] >= kSparseMinDegree) {
         const size_t nt = nnz + n + 8;

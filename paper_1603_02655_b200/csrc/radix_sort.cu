@@ -45,8 +45,9 @@ __device__ __forceinline__ uint64_t arc_key(uint32_t s, uint32_t d, uint64_t nv)
 template <bool ARCS>
 __global__ void __launch_bounds__(kRsThreads)
 rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask, int radix,
-           uint32_t *__restrict__ hist, size_t ntiles, ArcSource a) {
+           uint32_t *__restrict__ hist, size_t ntiles, ArcSource a, const uint32_t *dn) {
     __shared__ uint32_t h[kMaxRadix];
+    if (dn) n = min(n, (size_t)*dn);   // device-side key count (tiles past it count zero)
     for (int i = threadIdx.x; i < radix; i += kRsThreads) h[i] = 0;
     __syncthreads();
     const size_t base = (size_t)blockIdx.x * kRsTile;
@@ -172,8 +173,12 @@ template <int BITS, bool ARCS>
 __global__ void __launch_bounds__(kDsThreads, 4)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
              uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles,
-             const uint32_t *__restrict__ totals, ArcSource a) {
+             const uint32_t *__restrict__ totals, ArcSource a, const uint32_t *dn) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (dn) {
+        n = min(n, (size_t)*dn);
+        if ((size_t)blockIdx.x * kRsTile >= n) return;   // block-uniform
+    }
     DownSmem &S = *reinterpret_cast<DownSmem *>(smem_raw);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kDsWarps * radix; i += kDsThreads) S.wc[i / radix][i % radix] = 0;
@@ -233,7 +238,7 @@ rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size
 }
 
 typedef void (*DownFn)(const uint64_t *, uint64_t *, size_t, int, uint32_t, int, const uint32_t *,
-                       size_t, const uint32_t *, ArcSource);
+                       size_t, const uint32_t *, ArcSource, const uint32_t *);
 #define TC_DS(A) {nullptr, rs_downsweep<1, A>, rs_downsweep<2, A>, rs_downsweep<3, A>,       \
                   rs_downsweep<4, A>, rs_downsweep<5, A>, rs_downsweep<6, A>,            \
                   rs_downsweep<7, A>, rs_downsweep<8, A>}
@@ -242,7 +247,8 @@ typedef void (*DownFn)(const uint64_t *, uint64_t *, size_t, int, uint32_t, int,
 
 tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
                          const RadixPass *passes, int npasses, cudaStream_t s,
-                         uint64_t *launches, uint64_t **sorted, const ArcSource *arcs) {
+                         uint64_t *launches, uint64_t **sorted, const ArcSource *arcs,
+                         const uint32_t *dn) {
     *sorted = keys;
     if (n <= 1 || npasses == 0) return TC_OK;
     if (n >= (1ull << 32)) {
@@ -288,16 +294,16 @@ tc_status radix_sort_u64(Mem &mem, uint64_t *keys, uint64_t *tmp, size_t n,
         const bool from_arcs = arcs && p == 0;
         if (from_arcs)
             rs_upsweep<true><<<(unsigned)ntiles, kRsThreads, 0, s>>>(
-                src, n, passes[p].shift, mask, radix, hist.p, ntiles, *arcs);
+                src, n, passes[p].shift, mask, radix, hist.p, ntiles, *arcs, dn);
         else
             rs_upsweep<false><<<(unsigned)ntiles, kRsThreads, 0, s>>>(
-                src, n, passes[p].shift, mask, radix, hist.p, ntiles, none);
+                src, n, passes[p].shift, mask, radix, hist.p, ntiles, none, dn);
         TC_CUDA(cudaGetLastError());
         rs_scan_digits<<<(unsigned)radix, 256, 0, s>>>(hist.p, ntiles, totals.p);
         TC_CUDA(cudaGetLastError());
         kDown[from_arcs][bits]<<<(unsigned)ntiles, kDsThreads, sizeof(DownSmem), s>>>(
             src, dst, n, passes[p].shift, mask, radix, hist.p, ntiles, totals.p,
-            from_arcs ? *arcs : none);
+            from_arcs ? *arcs : none, dn);
         TC_CUDA(cudaGetLastError());
         if (launches) *launches += 3;
         uint64_t *t = src;

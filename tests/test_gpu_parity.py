@@ -368,3 +368,45 @@ def test_concurrent_census_on_shared_graph(tcb):
             assert part == og.census_range(b, e)
     assert g.launches() > 0 and g.profile_get()["census_ms"] > 0
     g.close()
+
+
+def _row_lengths_graph(lengths, n, seed):
+    """Vertices 0..len(lengths)-1 get upper rows of exactly the given lengths
+    (random targets above them, random directions, some arcs duplicated or
+    reciprocated -- duplicates and mutual pairs sit in the row as extra keys
+    of one (row, max) run), over a sparse random background."""
+    rng = np.random.default_rng(seed)
+    src, dst = [], []
+    for u, L in enumerate(lengths):           # row u: exactly L canonical keys
+        k = L // 5
+        w = rng.choice(np.arange(u + 1, n), size=L - k, replace=False)
+        fwd = rng.random(L - k) < 0.5
+        src += list(np.where(fwd, u, w)); dst += list(np.where(fwd, w, u))
+        extra = rng.choice(w, size=k, replace=False)       # duplicates / reciprocations
+        rev = rng.random(k) < 0.5
+        src += list(np.where(rev, extra, u)); dst += list(np.where(rev, u, extra))
+    bg = synth.random_digraph(n, 4.0 / n, seed=seed + 1)
+    keep = np.minimum(bg.src, bg.dst) >= len(lengths)     # background leaves those rows alone
+    src = np.concatenate([np.array(src, np.uint32), bg.src[keep]])
+    dst = np.concatenate([np.array(dst, np.uint32), bg.dst[keep]])
+    perm = rng.permutation(src.size)
+    return synth.Arcs(n, src[perm], dst[perm])
+
+
+@pytest.mark.parametrize("lengths", [
+    [31, 32, 33, 1, 2, 63, 64, 65, 30, 34],          # short/long boundary, chunk crossings
+    [5] * 40 + [29, 3, 31, 7, 32, 32, 33],           # many short rows across 32-key chunks
+    [700, 1000, 1024, 12, 300],                       # long rows up to the shared-memory bound
+    [1025, 40, 3],                                    # one row above it: the full-LSD path
+])
+def test_row_sort_lengths_vs_oracle(tcb, lengths):
+    """a1 row sort (csr_build.cu k_row_sort / k_row_sort_long): rows of
+    exactly 32 / 33 / 1024 / 1025 canonical keys, rows crossing the 32-key
+    chunks, duplicates and mutual pairs inside a row; census and stats equal
+    the oracle's."""
+    for seed in range(3):
+        a = _row_lengths_graph(lengths, 3000, seed)
+        c, st = gpu_census(tcb, a)
+        g = oracle.Graph(a.n, a.src, a.dst)
+        assert c == g.census(), (lengths, seed)
+        assert st == g.stats(), (lengths, seed)
