@@ -11,12 +11,12 @@
 //                (strict digraph); computed by the first radix
 //                pass straight from the arc list, which also counts them.
 //   2. sort      LSD radix sort (radix_sort.cu) on the min (row) bits, then
-//                a row sort (k_row_sort: shuffle ranking for rows <= 32 keys,
-//                a shared-memory bitonic network up to kRowMed) by the max
-//                bits: canonical pairs in the algorithm's own dyad order (u
-//                ascending, v ascending).  Graphs with a row of
-//                more than kRowMed keys take the full LSD (max bits, then min
-//                bits) instead.
+//                a row sort by the max bits (bitonic networks per row, in
+//                registers for rows <= 64 keys, in shared memory up to
+//                kRowMed): canonical pairs in the algorithm's own dyad order (u
+//                ascending, v ascending).  Rows of more than
+//                kRowMed keys are sorted together by one LSD (max bits, row
+//                bits) of their keys (k_huge_rows).
 //   3. compact   a ballot/popc compaction keeps the first key of each (min,
 //                max) run with the OR of the run's direction bits (dedup +
 //                mutual merge): the canonical dyad list dyad_u / dyad_e (the
@@ -135,38 +135,57 @@ __device__ __forceinline__ bool chunk_head(const HeadChunk &c, int r, size_t L, 
 //                   row's low words in registers through a bitonic network
 //   k_row_sort_warp rows of 33..kRowMed keys: one warp per row, a bitonic
 //                   network over the low words in shared memory
-// Rows of more than kRowMed keys are only counted: the host then reruns the
-// full LSD (max bits, then min bits) instead (hub graphs).
+// Rows of more than kRowMed keys (hub rows) are gathered into one array of
+// (row-list index, low word) keys, LSD-sorted and scattered back.
 // Keys equal in (row, max) are duplicates or the two arcs of a mutual pair;
 // the compaction merges them in any order.
 // ---------------------------------------------------------------------------
 constexpr int kRowMed = 1024;
-constexpr int kRowClasses = 5;   // <= 8, <= 16, <= 32, <= kRowMed, larger
+constexpr int kRowClasses = 6;   // <= 8, <= 16, <= 32, <= 64, <= kRowMed, larger
 
+// two keys per thread (one 16-byte load); a row start / end writes its
+// position into rstart / rend of the row (rows ascend with the position)
 __global__ void k_row_bounds(const uint64_t *__restrict__ X, size_t m,
                              const unsigned long long *__restrict__ dropped,
                              uint32_t *__restrict__ rstart, uint32_t *__restrict__ rend) {
     const size_t L = m - *dropped;
     const uint32_t lane = threadIdx.x & 31;
-    const size_t p = (size_t)blockIdx.x * blockDim.x + threadIdx.x;   // one key per thread
-    if (p - lane >= L) return;   // warp-uniform
-    const uint32_t r = p < L ? (uint32_t)(__ldg(X + p) >> 32) : ~0u;
-    uint32_t prv = __shfl_up_sync(0xffffffffu, r, 1);
-    uint32_t nxt = __shfl_down_sync(0xffffffffu, r, 1);
-    if (lane == 0) prv = p ? (uint32_t)(__ldg(X + p - 1) >> 32) : ~r;
-    if (lane == 31) nxt = p + 1 < L ? (uint32_t)(__ldg(X + p + 1) >> 32) : ~r;
+    const size_t p = 2 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (p - 2 * lane >= L) return;   // warp-uniform
+    uint32_t r0 = ~0u, r1 = ~0u;
+    if (p + 1 < L) {
+        const ulonglong2 k = __ldg(reinterpret_cast<const ulonglong2 *>(X + p));
+        r0 = (uint32_t)(k.x >> 32);
+        r1 = (uint32_t)(k.y >> 32);
+    } else if (p < L) {
+        r0 = (uint32_t)(__ldg(X + p) >> 32);
+    }
+    uint32_t prv = __shfl_up_sync(0xffffffffu, r1, 1);
+    uint32_t nxt = __shfl_down_sync(0xffffffffu, r0, 1);
+    if (lane == 0) prv = p ? (uint32_t)(__ldg(X + p - 1) >> 32) : ~r0;
+    if (lane == 31) nxt = p + 2 < L ? (uint32_t)(__ldg(X + p + 2) >> 32) : ~r1;
     if (p < L) {
-        if (prv != r) rstart[r] = (uint32_t)p;
-        if (nxt != r) rend[r] = (uint32_t)(p + 1);
+        if (prv != r0) rstart[r0] = (uint32_t)p;
+        if (p + 1 < L) {
+            if (r1 != r0) {
+                rend[r0] = (uint32_t)(p + 1);
+                rstart[r1] = (uint32_t)(p + 1);
+            }
+            if (nxt != r1) rend[r1] = (uint32_t)(p + 2);
+        } else {
+            rend[r0] = (uint32_t)(p + 1);
+        }
     }
 }
 
 __device__ __forceinline__ int row_class(uint32_t len) {
-    return len <= 1 ? -1 : len <= 8 ? 0 : len <= 16 ? 1 : len <= 32 ? 2
-         : len <= (uint32_t)kRowMed ? 3 : 4;
+    return len <= 1 ? -1 : len <= 8 ? 0 : len <= 16 ? 1 : len <= 32 ? 2 : len <= 64 ? 3
+         : len <= (uint32_t)kRowMed ? 4 : 5;
 }
 
-// lists: kRowClasses arrays of n entries each; cnt[c] = entries of class c.
+// lists: kRowClasses arrays of n entries each; cnt[c] = entries of class c,
+// cnt[kRowClasses] / cnt[kRowClasses + 1] = keys in rows of more than 64 /
+// more than kRowMed keys.
 // Each block takes one contiguous range of vertices: it counts its classes,
 // reserves them with one atomic per class (no contention on the counters),
 // then writes its entries (vertex order inside the block's share).
@@ -182,9 +201,13 @@ k_row_classify(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__
     if (threadIdx.x < kRcThreads / 32 * kRowClasses) (&wcnt[0][0])[threadIdx.x] = 0;
     __syncthreads();
     // pass 1: per-warp class counts over the block's range
-    uint32_t c_loc[kRowClasses] = {0, 0, 0, 0, 0};
+    uint32_t c_loc[kRowClasses] = {0, 0, 0, 0, 0, 0};
+    unsigned long long long_keys = 0, huge_keys = 0;   // keys in rows of > 64 / > kRowMed
     for (uint64_t u = u0 + threadIdx.x; u < u1; u += kRcThreads) {
-        const int c = row_class(__ldg(rend + u) - __ldg(rstart + u));
+        const uint32_t len = __ldg(rend + u) - __ldg(rstart + u);
+        const int c = row_class(len);
+        long_keys += len > 64 ? len : 0;
+        huge_keys += len > (uint32_t)kRowMed ? len : 0;
 #pragma unroll
         for (int k = 0; k < kRowClasses; k++) c_loc[k] += c == k;
     }
@@ -193,6 +216,10 @@ k_row_classify(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__
         const uint32_t t = __reduce_add_sync(0xffffffffu, c_loc[k]);
         if (lane == 0) wcnt[warp][k] = t;
     }
+    long_keys = warp_sum64(long_keys);
+    huge_keys = warp_sum64(huge_keys);
+    if (lane == 0 && long_keys) atomicAdd(&cnt[kRowClasses], long_keys);
+    if (lane == 0 && huge_keys) atomicAdd(&cnt[kRowClasses + 1], huge_keys);
     __syncthreads();
     if (threadIdx.x < kRowClasses) {
         uint32_t t = 0;
@@ -227,44 +254,100 @@ k_row_classify(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__
     }
 }
 
-// one thread per row of <= P keys: bitonic network over the low words
+// one thread per row of <= P keys: bitonic network over the row's low words
+// in registers (the row key is the same for all)
 template <int P>
-__global__ void __launch_bounds__(128)
-k_row_sort_net(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
+__device__ __forceinline__ void sort_row_regs(uint64_t *__restrict__ X, uint32_t u, uint32_t s0,
+                                              uint32_t len) {
+    uint32_t v[P];
+#pragma unroll
+    for (int j = 0; j < P; j++) v[j] = j < (int)len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
+#pragma unroll
+    for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+        for (int h = k >> 1; h > 0; h >>= 1) {
+#pragma unroll
+            for (int j = 0; j < P; j++) {
+                const int x = j ^ h;
+                if (x > j) {
+                    const uint32_t a = v[j], b = v[x];
+                    const bool up = (j & k) == 0;
+                    v[j] = up ? min(a, b) : max(a, b);
+                    v[x] = up ? max(a, b) : min(a, b);
+                }
+            }
+        }
+    }
+    const uint64_t hi = (uint64_t)u << 32;
+#pragma unroll
+    for (int j = 0; j < P; j++)
+        if (j < (int)len) X[s0 + j] = hi | v[j];
+}
+
+// classes 0..2 (rows of 2..32 keys) in one launch: block b belongs to the
+// class whose block range holds it (class c has ceil(cnt[c] / 128) blocks)
+constexpr int kRssThreads = 128;
+__global__ void __launch_bounds__(kRssThreads)
+k_row_sort_small(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
+                 const uint32_t *__restrict__ rend, const uint32_t *__restrict__ lists, uint64_t n,
+                 const unsigned long long *__restrict__ cnt) {
+    uint64_t b = blockIdx.x;
+    int c = 0;
+    for (; c < 3; c++) {
+        const uint64_t nb = (cnt[c] + kRssThreads - 1) / kRssThreads;
+        if (b < nb) break;
+        b -= nb;
+    }
+    if (c == 3) return;   // block-uniform
+    const uint64_t i = b * kRssThreads + threadIdx.x;
+    if (i >= cnt[c]) return;
+    const uint32_t u = __ldg(lists + (size_t)c * n + i);
+    const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
+    if (c == 0) sort_row_regs<8>(X, u, s0, len);
+    else if (c == 1) sort_row_regs<16>(X, u, s0, len);
+    else sort_row_regs<32>(X, u, s0, len);
+}
+
+// class 3 (33..64 keys): one warp per row, two elements per lane, bitonic
+// network across lanes by shuffles
+__global__ void __launch_bounds__(256)
+k_row_sort_w64(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
                const uint32_t *__restrict__ rend, const uint32_t *__restrict__ list,
                const unsigned long long *__restrict__ cnt) {
     const uint64_t nr = *cnt;
-    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nr;
-         i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < nr; i += nw) {
         const uint32_t u = __ldg(list + i);
         const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
-        uint32_t v[P];
-#pragma unroll
-        for (int j = 0; j < P; j++) v[j] = j < (int)len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
-#pragma unroll
-        for (int k = 2; k <= P; k <<= 1) {
-#pragma unroll
-            for (int h = k >> 1; h > 0; h >>= 1) {
-#pragma unroll
-                for (int j = 0; j < P; j++) {
-                    const int x = j ^ h;
-                    if (x > j) {
-                        const uint32_t a = v[j], b = v[x];
-                        const bool up = (j & k) == 0;
-                        v[j] = up ? min(a, b) : max(a, b);
-                        v[x] = up ? max(a, b) : min(a, b);
-                    }
+        uint32_t e0 = lane < len ? (uint32_t)__ldg(X + s0 + lane) : ~0u;
+        uint32_t e1 = lane + 32 < len ? (uint32_t)__ldg(X + s0 + 32 + lane) : ~0u;
+    #pragma unroll
+        for (uint32_t k = 2; k <= 64; k <<= 1) {
+    #pragma unroll
+            for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+                if (h == 32) {   // pairs (lane, lane + 32), k = 64: ascending
+                    const uint32_t lo = min(e0, e1), hv = max(e0, e1);
+                    e0 = lo;
+                    e1 = hv;
+                } else {
+                    const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, h);
+                    const uint32_t o1 = __shfl_xor_sync(0xffffffffu, e1, h);
+                    // element index lane (+ 32): keep the min iff ascending == lower
+                    const bool lower = (lane & h) == 0;
+                    const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+                    e0 = (up0 == lower) ? min(e0, o0) : max(e0, o0);
+                    e1 = (up1 == lower) ? min(e1, o1) : max(e1, o1);
                 }
             }
         }
         const uint64_t hi = (uint64_t)u << 32;
-#pragma unroll
-        for (int j = 0; j < P; j++)
-            if (j < (int)len) X[s0 + j] = hi | v[j];
+        if (lane < len) X[s0 + lane] = hi | e0;
+        if (lane + 32 < len) X[s0 + 32 + lane] = hi | e1;
     }
 }
 
-// one warp per row of 33..kRowMed keys: bitonic network in shared memory
+// class 4 (65..kRowMed keys): one warp per row, bitonic network in shared memory
 constexpr int kRswThreads = 256;
 __global__ void __launch_bounds__(kRswThreads)
 k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
@@ -278,33 +361,6 @@ k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
     for (size_t i = ((size_t)blockIdx.x * kRswThreads + threadIdx.x) >> 5; i < nr; i += nw) {
         const uint32_t u = __ldg(list + i);
         const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
-        const uint64_t hi = (uint64_t)u << 32;
-        if (len <= 64) {   // two elements per lane, network across lanes by shuffles
-            uint32_t e0 = lane < len ? (uint32_t)__ldg(X + s0 + lane) : ~0u;
-            uint32_t e1 = lane + 32 < len ? (uint32_t)__ldg(X + s0 + 32 + lane) : ~0u;
-#pragma unroll
-            for (uint32_t k = 2; k <= 64; k <<= 1) {
-#pragma unroll
-                for (uint32_t h = k >> 1; h > 0; h >>= 1) {
-                    if (h == 32) {   // partner in the same lane: (lane, lane + 32), k = 64: ascending
-                        const uint32_t lo = min(e0, e1), hv = max(e0, e1);
-                        e0 = lo;
-                        e1 = hv;
-                    } else {
-                        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, e0, h);
-                        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, e1, h);
-                        // element index e = lane (+ 32); keep the min iff ascending == lower
-                        const bool lower = (lane & h) == 0;
-                        const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
-                        e0 = (up0 == lower) ? min(e0, o0) : max(e0, o0);
-                        e1 = (up1 == lower) ? min(e1, o1) : max(e1, o1);
-                    }
-                }
-            }
-            if (lane < len) X[s0 + lane] = hi | e0;
-            if (lane + 32 < len) X[s0 + 32 + lane] = hi | e1;
-            continue;
-        }
         uint32_t P = 128;
         while (P < len) P <<= 1;
         for (uint32_t j = lane; j < P; j += 32) b[j] = j < len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
@@ -322,8 +378,41 @@ k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
                 __syncwarp();
             }
         }
+        const uint64_t hi = (uint64_t)u << 32;
         for (uint32_t j = lane; j < len; j += 32) X[s0 + j] = hi | b[j];
         __syncwarp();
+    }
+}
+
+// rows of more than kRowMed keys (hub rows): gathered into one array of
+// composite keys (index of the row in the class list << 32 | low word), LSD
+// sorted on the max bits and then the row-index bits (radix_sort.cu), and
+// scattered back; hoff = exclusive prefix of the rows' lengths (list order)
+struct HugeLen {
+    const uint32_t *list, *rstart, *rend;
+    __device__ __forceinline__ uint32_t operator()(size_t i) const {
+        const uint32_t u = list[i];
+        return rend[u] - rstart[u];
+    }
+};
+
+template <bool GATHER>
+__global__ void k_huge_rows(uint64_t *__restrict__ X, uint64_t *__restrict__ S,
+                            const uint32_t *__restrict__ rstart, const uint32_t *__restrict__ list,
+                            const uint32_t *__restrict__ hoff, uint64_t nh, uint64_t ns) {
+    // one thread per element of S: its row i = last hoff[i] <= e (binary search)
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < ns;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t lo = 0, hi = nh;
+        while (hi - lo > 1) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (__ldg(hoff + mid) <= e) lo = mid;
+            else hi = mid;
+        }
+        const uint32_t u = __ldg(list + lo);
+        const uint64_t x = __ldg(rstart + u) + (e - __ldg(hoff + lo));
+        if (GATHER) S[e] = lo << 32 | (uint32_t)X[x];
+        else X[x] = (uint64_t)u << 32 | (uint32_t)S[e];
     }
 }
 
@@ -409,9 +498,17 @@ k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
 // the random L2 round trips overlap instead of serialising behind the
 // (possibly aliasing) ul[k] stores of the previous key.
 constexpr int kWlBatch = 4;
+// TC_WL_PARTS: the dyads are handled in that many launches by dyad-index
+// range [klo, khi) (the random ul[k] working set of one launch is D / parts
+// words, so it stays in L2 while the sorted keys stream past); the row starts
+// are written by the first launch
+#ifndef TC_WL_PARTS
+#define TC_WL_PARTS 1
+#endif
 __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *__restrict__ dD,
                               const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
-                              uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start) {
+                              uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start,
+                              uint32_t klo, uint32_t khi, int starts) {
     const size_t D = *dD;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < D;
@@ -427,19 +524,23 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *_
 #pragma unroll
         for (int j = 0; j < kWlBatch; j++) {
             const size_t i = i0 + j * stride;
-            us[j] = i < D ? __ldg(up_start + key_row(key[j])) : 0u;
-            val[j] = i < D ? ul[(uint32_t)key[j]] : 0u;
+            const uint32_t k = (uint32_t)key[j];
+            const bool mine = i < D && k >= klo && k < khi;
+            us[j] = mine ? __ldg(up_start + key_row(key[j])) : 0u;
+            val[j] = mine ? ul[k] : 0u;
         }
 #pragma unroll
         for (int j = 0; j < kWlBatch; j++) {
             const size_t i = i0 + j * stride;
             if (i >= D) continue;
             const uint32_t r = key_row(key[j]), k = (uint32_t)key[j];
-            const uint32_t pos = us[j] + r + (uint32_t)i;
-            adj[pos] = val[j];
-            ul[k] = pos + 1u;
+            if (k >= klo && k < khi) {
+                const uint32_t pos = us[j] + r + (uint32_t)i;
+                adj[pos] = val[j];
+                ul[k] = pos + 1u;
+            }
             const uint32_t prev = i ? key_row(prv[j]) : 0xffffffffu;
-            if (i == 0 || prev != r) {
+            if (starts && (i == 0 || prev != r)) {
                 const uint32_t first = i == 0 ? 0u : prev + 1;
                 for (uint32_t x = first; x <= r; x++) lo_start[x] = (uint32_t)i;
             }
@@ -515,7 +616,8 @@ __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
 // cost c = |N(u)| + |N(v)| (uniform workload); merge length
 // t = |{w in N(u): w > u}| + |{w in N(v): w > u}| (dpb from k_write_lower);
 // stats [2] = distinct arcs m, [3] = mutual dyads
-__global__ void k_write_upper(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
+__global__ void __launch_bounds__(256, 4)
+k_write_upper(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
                               const uint32_t *__restrict__ lo_start,
                               const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
                               const uint32_t *__restrict__ dpb, const uint32_t *__restrict__ dD,
@@ -626,24 +728,18 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         DevBuf<unsigned long long> rc;
         if ((st = rb.allocate(mem, 2 * (n + 1))) != TC_OK) return st;
         if ((st = lists.allocate(mem, (size_t)kRowClasses * n)) != TC_OK) return st;
-        if ((st = rc.allocate(mem, kRowClasses)) != TC_OK) return st;
+        if ((st = rc.allocate(mem, kRowClasses + 2)) != TC_OK) return st;
         uint32_t *rstart = rb.p, *rend = rb.p + n + 1;
         TC_CUDA(cudaMemsetAsync(rb.p, 0, 2 * (n + 1) * sizeof(uint32_t), s));
-        TC_CUDA(cudaMemsetAsync(rc.p, 0, kRowClasses * sizeof(unsigned long long), s));
-        k_row_bounds<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(sorted, m, scratch.p + 1, rstart,
+        TC_CUDA(cudaMemsetAsync(rc.p, 0, (kRowClasses + 2) * sizeof(unsigned long long), s));
+        k_row_bounds<<<(unsigned)((m + 511) / 512), 256, 0, s>>>(sorted, m, scratch.p + 1, rstart,
                                                                  rend);
         k_row_classify<<<grid_for(n, kRcThreads, 148 * 8), kRcThreads, 0, s>>>(rstart, rend, n,
                                                                          lists.p, rc.p);
-        const unsigned gnet = grid_for(n, 128, 148 * 64);
-        k_row_sort_net<8><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p, rc.p);
-        k_row_sort_net<16><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p + n, rc.p + 1);
-        k_row_sort_net<32><<<gnet, 128, 0, s>>>(sorted, rstart, rend, lists.p + 2 * n, rc.p + 2);
-        k_row_sort_warp<<<148 * 4, kRswThreads, 0, s>>>(sorted, rstart, rend, lists.p + 3 * n,
-                                                        rc.p + 3);
         TC_CUDA(cudaGetLastError());
-        g->launches += 6;
-        // host read: range check, and whether a row exceeded kRowMed keys
-        unsigned long long h0[2], rch[kRowClasses];
+        g->launches += 2;
+        // host read: range check, the row classes (hub graph or not)
+        unsigned long long h0[2], rch[kRowClasses + 2];
         TC_CUDA(cudaMemcpyAsync(h0, scratch.p, sizeof(h0), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaMemcpyAsync(rch, rc.p, sizeof(rch), cudaMemcpyDeviceToHost, s));
         TC_CUDA(cudaStreamSynchronize(s));
@@ -652,7 +748,10 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
             return TC_E_RANGE;
         }
         dropped_h = h0[1];
-        if (rch[kRowClasses - 1]) {   // hub rows: the full LSD, max bits then min bits, from the arcs again
+        if (5 * rch[kRowClasses] > m - dropped_h) {
+            // hub graph (more than a fifth of the keys in rows of > 64): the
+            // full LSD (max bits, then min bits) from the arcs again is cheaper
+            // than sorting the long rows (DESIGN 5.2)
             unsigned long long init2[2] = {~0ull, 0};
             TC_CUDA(cudaMemcpyAsync(scratch.p, init2, sizeof(init2), cudaMemcpyHostToDevice, s));
             np = radix_passes_for(2, b, passes);
@@ -660,6 +759,44 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
             if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
                                      &as)) != TC_OK)
                 return st;
+        } else {
+            k_row_sort_small<<<(unsigned)(n / kRssThreads + 3), kRssThreads, 0, s>>>(
+                sorted, rstart, rend, lists.p, n, rc.p);
+            const uint64_t n33 = n < m / 33 ? n : m / 33;   // rows of >= 33 keys
+            k_row_sort_w64<<<grid_for(n33 * 32, 256, 148 * 16), 256, 0, s>>>(
+                sorted, rstart, rend,
+                                                                       lists.p + 3 * n, rc.p + 3);
+            k_row_sort_warp<<<148 * 7, kRswThreads, 0, s>>>(sorted, rstart, rend,
+                                                            lists.p + 4 * n, rc.p + 4);
+            TC_CUDA(cudaGetLastError());
+            g->launches += 3;
+        }
+        if (5 * rch[kRowClasses] <= m - dropped_h && rch[kRowClasses - 1]) {
+            const uint64_t nh = rch[kRowClasses - 1];   // rows of > kRowMed keys
+            const uint32_t *hl = lists.p + (size_t)(kRowClasses - 1) * n;
+            const uint64_t ns = rch[kRowClasses + 1];
+            DevBuf<uint32_t> hoff;
+            if ((st = hoff.allocate(mem, nh)) != TC_OK) return st;
+            if ((st = scan_exclusive<uint32_t>(mem, nh, HugeLen{hl, rstart, rend},
+                                               ArrayOutExcl<uint32_t>{hoff.p}, (uint32_t *)nullptr,
+                                               s, &g->launches)) != TC_OK)
+                return st;
+            DevBuf<uint64_t> S, S2;
+            if ((st = S.allocate(mem, ns)) != TC_OK) return st;
+            if ((st = S2.allocate(mem, ns)) != TC_OK) return st;
+            const unsigned gh = grid_for(ns, 256, 148 * 16);
+            k_huge_rows<true><<<gh, 256, 0, s>>>(sorted, S.p, rstart, hl, hoff.p, nh, ns);
+            int hb = 1;
+            while (hb < 32 && (1ull << hb) < nh) hb++;
+            np = radix_passes_for(2, b, passes);
+            np += radix_passes_for(32, hb, passes + np);
+            uint64_t *ss = S.p;
+            if ((st = radix_sort_u64(mem, S.p, S2.p, ns, passes, np, s, &g->launches, &ss)) !=
+                TC_OK)
+                return st;
+            k_huge_rows<false><<<gh, 256, 0, s>>>(sorted, ss, rstart, hl, hoff.p, nh, ns);
+            TC_CUDA(cudaGetLastError());
+            g->launches += 2;
         }
     } else if (m == 1) {
         k_emit<<<1, 32, 0, s>>>(d_src, d_dst, m, n, keys.p, scratch.p);
@@ -754,9 +891,14 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         return TC_E_OOM;
     }
     if (Dub) {
-        k_write_lower<<<grid_for(Dub, 256), 256, 0, s>>>(tsorted, total.p, up_start.p, adj, dpb,
-                                                         lo_start.p);
-        g->launches += 1;
+        const uint64_t per = (Dub + TC_WL_PARTS - 1) / TC_WL_PARTS;
+        for (int part = 0; part < TC_WL_PARTS; part++) {
+            const uint64_t klo = per * part, khi = per * (part + 1);
+            k_write_lower<<<grid_for(Dub, 256), 256, 0, s>>>(
+                tsorted, total.p, up_start.p, adj, dpb, lo_start.p, (uint32_t)klo,
+                (uint32_t)(khi < 0xffffffffull ? khi : 0xffffffffull), part == 0);
+        }
+        g->launches += TC_WL_PARTS;
     }
     k_fill_tail_last<<<grid_for(n + 1, 256), 256, 0, s>>>(lo_start.p, tsorted, total.p, n);
     k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj,
