@@ -191,7 +191,7 @@ void tc_graph_destroy(tc_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
     g->mem.free(g->off, g->off_n * 4);
-    g->mem.free(g->adj, g->adj_n * 4);
+    g->mem.free(g->adj, (g->adj_alloc_n ? g->adj_alloc_n : g->adj_n) * 4);
     g->mem.free(g->dyad_u, g->dyad_n * 4);
     g->mem.free(g->dyad_e, g->dyad_n * 4);
     g->mem.free(g->dyad_c, g->dyad_n * 4);
@@ -199,6 +199,10 @@ void tc_graph_destroy(tc_graph *g) {
     g->mem.free(g->dyad_t, g->dyad_n * 4);
     g->mem.free(g->ups, g->ups_n * 4);
     if (g->tagpre) g->mem.free(g->tagpre, g->tagpre_n * 8);
+    g->mem.free(g->plan_items, g->plan_cap_tiles * tc::kPlanTileItems * sizeof(tc::BinItemT));
+    g->mem.free(g->plan_tcount, g->plan_cap_tiles * 4);
+    g->mem.free(g->plan_big, g->plan_cap_big * 4);
+    g->mem.free(g->plan_sums, 8 * 8);
     cudaStreamSynchronize(g->stream);
     delete g;
 }

@@ -22,6 +22,7 @@ constexpr int kCensusThreads = 256;
 constexpr int kPlanThreads = 256;
 constexpr int kPlanItems = 16;
 constexpr int kPlanTile = kPlanThreads * kPlanItems;   // canonical dyads per plan tile
+static_assert(kPlanTile == kPlanTileItems, "plan tile size");
 
 
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]

@@ -34,7 +34,9 @@
 //   6. stats     m, mutual dyads, sum d^2, max degree, per-dyad cost c,
 //                where the entries w > u of row v start (dyad_pb: one past
 //                the lower entry u of row v) and the merge length t
-//                (census.cu).
+//                (census.cu); the upper entries, c and t are written by
+//                schedule.cu k_upper_plan, which also stores the graph's
+//                full-census plan (thread-bin items sorted by t per tile).
 // Sorting one key per arc and D transposed keys (instead of both
 // orientations of every arc) cuts the sort work by a quarter and halves the
 // compaction.
@@ -611,64 +613,10 @@ __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
 }
 
 
-// upper entries + per-dyad data, one thread per canonical dyad k = (u, v):
-// the entry of v goes to ups[u] + (k - up_start[u]) = lo_start[u+1] + u + k;
-// cost c = |N(u)| + |N(v)| (uniform workload); merge length
-// t = |{w in N(u): w > u}| + |{w in N(v): w > u}| (dpb from k_write_lower);
-// stats [2] = distinct arcs m, [3] = mutual dyads
-__global__ void __launch_bounds__(256, 4)
-k_write_upper(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ups,
-                              const uint32_t *__restrict__ lo_start,
-                              const uint32_t *__restrict__ du, const uint32_t *__restrict__ de,
-                              const uint32_t *__restrict__ dpb, const uint32_t *__restrict__ dD,
-                              uint32_t *__restrict__ adj, uint32_t *__restrict__ dc,
-                              uint32_t *__restrict__ dt, unsigned long long *out) {
-    const uint64_t D = *dD;
-    unsigned long long m = 0, mu = 0;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    // kWlBatch dyads per thread, all loads (the random off[v], off[v+1] among
-    // them) issued before the stores
-    for (uint64_t k0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; k0 < D;
-         k0 += kWlBatch * stride) {
-        uint32_t u[kWlBatch], e[kWlBatch], pb[kWlBatch], ls[kWlBatch], ou[kWlBatch],
-            ou1[kWlBatch], ov[kWlBatch], ov1[kWlBatch], up[kWlBatch];
-#pragma unroll
-        for (int j = 0; j < kWlBatch; j++) {
-            const uint64_t k = k0 + j * stride;
-            const bool ok = k < D;
-            u[j] = ok ? __ldg(du + k) : 0u;
-            e[j] = ok ? __ldg(de + k) : 0u;
-            pb[j] = ok ? dpb[k] : 0u;
-        }
-#pragma unroll
-        for (int j = 0; j < kWlBatch; j++) {
-            const uint32_t v = e[j] >> 2;
-            ls[j] = __ldg(lo_start + u[j] + 1);
-            ou[j] = __ldg(off + u[j]);
-            ou1[j] = __ldg(off + u[j] + 1);
-            up[j] = __ldg(ups + u[j]);
-            ov[j] = __ldg(off + v);
-            ov1[j] = __ldg(off + v + 1);
-        }
-#pragma unroll
-        for (int j = 0; j < kWlBatch; j++) {
-            const uint64_t k = k0 + j * stride;
-            if (k >= D) continue;
-            adj[ls[j] + u[j] + (uint32_t)k] = e[j];
-            dc[k] = (ou1[j] - ou[j]) + (ov1[j] - ov[j]) - 2;
-            dt[k] = (ou1[j] - 1 - up[j]) + (ov1[j] - 1 - pb[j]);
-            const uint32_t t = e[j] & 3u;
-            m += __popc(t);
-            mu += (t == 3u);
-        }
-    }
-    m = warp_sum64(m);
-    mu = warp_sum64(mu);
-    if ((threadIdx.x & 31) == 0) {
-        if (m) atomicAdd(&out[2], m);
-        if (mu) atomicAdd(&out[3], mu);
-    }
-}
+// upper entries + per-dyad data (c, t, arc / mutual stats): schedule.cu
+// k_upper_plan, fused with the tile-local length sort of the census plan
+// (entry of v in row u at lo_start[u+1] + u + k; c = |N(u)| + |N(v)|, P:1693;
+// t = entries > u of both rows, census.cu)
 
 // (tag == 1) << 32 | (tag == 2) of adj entry i (sentinels count as tag 3)
 struct TagIn {
@@ -886,6 +834,7 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     // then offsets, sentinels and vertex stats, then upper entries
     uint32_t *adj = (uint32_t *)mem.alloc((2ull * Dub + n + 8) * sizeof(uint32_t));
     g->adj = adj;
+    g->adj_alloc_n = 2ull * Dub + n + 8;
     if (!adj) {
         set_error("device allocation for the CSR failed");
         return TC_E_OOM;
@@ -904,11 +853,12 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     k_offsets<<<grid_for(n + 9, 256), 256, 0, s>>>(lo_start.p, up_start.p, n, off, ups, adj,
                                                    scratch.p + 4);
     g->launches += 2;
-    if (Dub) {
-        k_write_upper<<<grid_for(Dub, 256), 256, 0, s>>>(off, ups, lo_start.p, du, de, dpb,
-                                                         total.p, adj, dc, dt, scratch.p + 4);
-        g->launches += 1;
-    }
+    // the sort buffers are dead from here on (stream-ordered frees)
+    keys.release();
+    tmp.release();
+    // upper entries, c, t, and the graph's own full-census plan (schedule.cu)
+    if ((st = upper_plan_device(g, lo_start.p, total.p, Dub, scratch.p + 4, s)) != TC_OK)
+        return st;
     TC_CUDA(cudaGetLastError());
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));

@@ -411,6 +411,265 @@ k_range_dyadic(const uint32_t *__restrict__ off, const uint32_t *__restrict__ ad
         atomicAdd(&d_counts[threadIdx.x], part[threadIdx.x]);
 }
 
+// ---------------------------------------------------------------------------
+// Full-census plan built with the graph (a1 + a2 fused, round 2).  The CSR
+// builder's last assembly step (upper row entries, per-dyad c and t) runs
+// here tile by tile; while a tile's merge lengths are in registers they are
+// ranked exactly as k_plan_tile ranks them, and the thread-bin items of the
+// whole dyad range [0, D) are stored with the graph, together with the list
+// of big dyads (t > kThreadBinMax), the dyadic base sums n - c per pre and the
+// thread-bin work sums.  A full 16-class census then only turns the big
+// dyads into warp items (k_emit_big) and runs the bin kernels; dyad ranges,
+// shards and the 64-type census keep the per-call plan (k_plan_tile).
+// sums: [0..2] n - c of pre 1..3, [3] thread-bin sum of c, [4] thread-bin
+// sum of t, [5] big dyads (the length of `big`)
+// ---------------------------------------------------------------------------
+struct UpperIn {
+    const uint32_t *off, *ups, *lo_start, *du, *de, *dpb, *dD;
+    uint32_t *adj, *dc, *dt;
+    uint64_t n;
+};
+
+#ifndef TC_UP_BATCH
+#define TC_UP_BATCH 4
+#endif
+constexpr int kUpBatch = TC_UP_BATCH;   // dyads per thread whose loads are in flight together
+
+#ifndef TC_UP_MINB
+#define TC_UP_MINB 4
+#endif
+__global__ void __launch_bounds__(kPlanThreads, TC_UP_MINB)
+k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ tile_count,
+             uint32_t *__restrict__ big, unsigned long long *__restrict__ sums,
+             unsigned long long *__restrict__ bstats /* [2] += arcs, [3] += mutual dyads */) {
+    __shared__ uint32_t wc[kPlanWarps][kDigits];
+    __shared__ uint16_t perm[kPlanTile];
+    __shared__ uint32_t wbig[kPlanWarps];
+    __shared__ unsigned long long big_base;
+    const uint64_t N = *I.dD;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * kPlanTile;
+    if (tile0 >= N) return;   // block-uniform
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kPlanWarps * kDigits; i += kPlanThreads) (&wc[0][0])[i] = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    const uint32_t wbase = warp * 32 * kPlanItems;
+    // per dyad: its length digit in shared memory (phase 1 keeps no per-dyad
+    // registers, so more loads stay in flight), its rank in 16-bit halves of rk
+    __shared__ uint8_t dgs[kPlanTile];
+    uint32_t rk[kPlanItems / 2];
+    uint32_t m = 0, mu = 0, tt = 0;
+    unsigned long long dy1 = 0, dy2 = 0, dy3 = 0, wt = 0;
+    // 1. the upper entries, c and t of the tile's dyads (k_write_upper's work)
+#pragma unroll 1
+    for (int kb = 0; kb < kPlanItems; kb += kUpBatch) {
+        uint32_t u[kUpBatch], e[kUpBatch], pb[kUpBatch];
+#pragma unroll
+        for (int j = 0; j < kUpBatch; j++) {
+            const uint64_t i = tile0 + wbase + (kb + j) * 32 + lane;
+            const bool ok = i < N;
+            u[j] = ok ? __ldg(I.du + i) : 0u;
+            e[j] = ok ? __ldg(I.de + i) : 0u;
+            pb[j] = ok ? __ldg(I.dpb + i) : 0u;
+        }
+        uint32_t ls[kUpBatch], ou[kUpBatch], ou1[kUpBatch], up[kUpBatch], ov[kUpBatch],
+            ov1[kUpBatch];
+#pragma unroll
+        for (int j = 0; j < kUpBatch; j++) {
+            const uint32_t v = e[j] >> 2;
+            ls[j] = __ldg(I.lo_start + u[j] + 1);
+            ou[j] = __ldg(I.off + u[j]);
+            ou1[j] = __ldg(I.off + u[j] + 1);
+            up[j] = __ldg(I.ups + u[j]);
+            ov[j] = __ldg(I.off + v);
+            ov1[j] = __ldg(I.off + v + 1);
+        }
+#pragma unroll
+        for (int j = 0; j < kUpBatch; j++) {
+            const uint64_t i = tile0 + wbase + (kb + j) * 32 + lane;
+            if (i >= N) {
+                dgs[wbase + (kb + j) * 32 + lane] = 0;
+                continue;
+            }
+            I.adj[ls[j] + u[j] + (uint32_t)i] = e[j];
+            const uint32_t c = (ou1[j] - ou[j]) + (ov1[j] - ov[j]) - 2;
+            const uint32_t t = (ou1[j] - 1 - up[j]) + (ov1[j] - 1 - pb[j]);
+            I.dc[i] = c;
+            I.dt[i] = t;
+            dgs[wbase + (kb + j) * 32 + lane] = (uint8_t)digit_of(t);
+            const uint32_t pre = e[j] & 3u;
+            m += __popc(pre);
+            mu += pre == 3u;
+            const unsigned long long dy = I.n - c;
+            dy1 += pre == 1u ? dy : 0ull;
+            dy2 += pre == 2u ? dy : 0ull;
+            dy3 += pre == 3u ? dy : 0ull;
+            if (t <= kThreadBinMax) {
+                wt += c;
+                tt += t;
+            }
+        }
+    }
+    __syncthreads();
+    // 2. stable rank by merge length (k_plan_tile's ballot ranking); big dyads counted
+    uint32_t nbw = 0;
+#pragma unroll
+    for (int k = 0; k < kPlanItems; k++) {
+        const uint64_t i = tile0 + wbase + k * 32 + lane;
+        const bool valid = i < N;
+        const uint32_t d = valid ? (uint32_t)dgs[wbase + k * 32 + lane] : 0x10000u;
+        uint32_t peers = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+        for (int bit = 0; bit < 8; bit++) {
+            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
+            peers &= ((d >> bit) & 1u) ? b : ~b;
+        }
+        uint32_t r = 0;
+        if (valid) r = wc[warp][d] + __popc(peers & lt);
+        __syncwarp();
+        if (valid && (peers & lt) == 0) wc[warp][d] += __popc(peers);
+        __syncwarp();
+        if (k & 1) rk[k >> 1] |= r << 16;
+        else rk[k >> 1] = r;
+        nbw += __popc(__ballot_sync(0xffffffffu, valid && d == 255u));
+    }
+    if (lane == 0) wbig[warp] = nbw;
+    __syncthreads();
+    uint32_t all;
+    {
+        const int d = threadIdx.x;
+        uint32_t tot = 0;
+#pragma unroll
+        for (int w = 0; w < kPlanWarps; w++) tot += wc[w][d];
+        if (d == 255) tot = 0;      // big dyads are not in the thread list
+        uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
+        if (d == 0) tile_count[blockIdx.x] = all;
+#pragma unroll
+        for (int w = 0; w < kPlanWarps; w++) {
+            uint32_t c = wc[w][d];
+            wc[w][d] = run;
+            run += c;
+        }
+        if (d == 0) {   // one reservation per block in the big-dyad list
+            uint32_t nb = 0;
+            for (int w = 0; w < kPlanWarps; w++) nb += wbig[w];
+            big_base = nb ? atomicAdd(&sums[5], (unsigned long long)nb) : 0ull;
+        }
+    }
+    __syncthreads();
+    uint64_t bpos = big_base;
+    for (int w = 0; w < warp; w++) bpos += wbig[w];
+#pragma unroll
+    for (int k = 0; k < kPlanItems; k++) {
+        const uint64_t i = tile0 + wbase + k * 32 + lane;
+        const bool valid = i < N;
+        const uint32_t d = dgs[wbase + k * 32 + lane];
+        const uint32_t r = (rk[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        if (valid && d < 255u) perm[wc[warp][d] + r] = (uint16_t)(wbase + k * 32 + lane);
+        const uint32_t bb = __ballot_sync(0xffffffffu, valid && d == 255u);
+        if (valid && d == 255u) big[bpos + __popc(bb & lt)] = (uint32_t)i;
+        bpos += __popc(bb);
+    }
+    __syncthreads();
+    // 3. the tile's thread-bin items in length order, stored coalesced
+    uint4 *out = reinterpret_cast<uint4 *>(tl + tile0);
+    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) {
+        const uint64_t i = tile0 + perm[j];
+        const uint32_t u = __ldg(I.du + i);
+        const uint32_t pa = __ldg(I.ups + u), a = __ldg(I.off + u + 1) - 1u - pa;
+        out[j] = make_uint4(pa, __ldg(I.dpb + i), __ldg(I.de + i), I.dt[i] | a << 16);
+    }
+    m = __reduce_add_sync(0xffffffffu, m);
+    mu = __reduce_add_sync(0xffffffffu, mu);
+    tt = __reduce_add_sync(0xffffffffu, tt);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        dy1 += __shfl_xor_sync(0xffffffffu, dy1, o);
+        dy2 += __shfl_xor_sync(0xffffffffu, dy2, o);
+        dy3 += __shfl_xor_sync(0xffffffffu, dy3, o);
+        wt += __shfl_xor_sync(0xffffffffu, wt, o);
+    }
+    if (lane == 0) {
+        if (m) atomicAdd(&bstats[2], (unsigned long long)m);
+        if (mu) atomicAdd(&bstats[3], (unsigned long long)mu);
+        if (dy1) atomicAdd(&sums[0], dy1);
+        if (dy2) atomicAdd(&sums[1], dy2);
+        if (dy3) atomicAdd(&sums[2], dy3);
+        if (wt) atomicAdd(&sums[3], wt);
+        if (tt) atomicAdd(&sums[4], (unsigned long long)tt);
+    }
+}
+
+// per full census: the big dyads of the graph's list become warp items
+// (merge chunks or skewed-pair items, as in k_plan_tile); block 0 also adds
+// the graph's dyadic base sums to the census and its thread-bin work sums to
+// the per-call stats (stats layout of census_range_device)
+template <bool SPARSE>
+__global__ void __launch_bounds__(256)
+k_emit_big(const PlanIn P, const uint32_t *__restrict__ big, const unsigned long long *__restrict__ sums,
+           BinItemW *__restrict__ wl, unsigned long long *__restrict__ stats,
+           unsigned long long *__restrict__ d_counts) {
+    const uint64_t nb = sums[5];
+    const uint32_t lane = threadIdx.x & 31;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        if (sums[0] + sums[1]) atomicAdd(&d_counts[1], sums[0] + sums[1]);
+        if (sums[2]) atomicAdd(&d_counts[2], sums[2]);
+        atomicAdd(&stats[1], sums[3]);
+        atomicAdd(&stats[4], sums[4]);
+        atomicAdd(&stats[3], nb);
+    }
+    unsigned long long ww = 0, tw = 0, nsp = 0, spc = 0, spu = 0;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t q0 = (uint64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31u); q0 < nb; q0 += stride) {
+        const uint64_t q = q0 + lane;
+        const bool valid = q < nb;
+        uint32_t nch = 0, smode = 0, span = 0, i = 0;
+        if (valid) {
+            i = __ldg(big + q);
+            const uint32_t c = __ldg(P.dt + i), cf = __ldg(P.dc + i);
+            uint32_t slen = 0, sunits = 0;
+            smode = SPARSE ? sparse_mode(P, i, &slen, &sunits) : 0u;
+            spu += smode ? sunits : 0u;
+            nch = smode ? max(1u, (slen + kSparseChunk - 1) / kSparseChunk)
+                        : (c + kWarpChunk - 1) / kWarpChunk;
+            ww += cf;
+            tw += c;
+            nsp += smode ? 1u : 0u;
+            spc += smode ? cf : 0u;
+            span = smode ? slen : c;
+        }
+        uint32_t incl = nch;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        const uint32_t wtot = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long at = 0;
+        if (lane == 31 && wtot) at = atomicAdd(&stats[0], (unsigned long long)wtot);
+        at = __shfl_sync(0xffffffffu, at, 31) + (incl - nch);
+        const uint32_t chunk = smode ? kSparseChunk : kWarpChunk;
+        for (uint32_t c = 0; c < nch; c++) {
+            const uint32_t d0 = c * chunk;
+            wl[at + c] = BinItemW{i, d0, min(span, d0 + chunk), smode};
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        ww += __shfl_xor_sync(0xffffffffu, ww, o);
+        tw += __shfl_xor_sync(0xffffffffu, tw, o);
+        nsp += __shfl_xor_sync(0xffffffffu, nsp, o);
+        spc += __shfl_xor_sync(0xffffffffu, spc, o);
+        spu += __shfl_xor_sync(0xffffffffu, spu, o);
+    }
+    if (lane == 0) {
+        if (ww) atomicAdd(&stats[2], ww);
+        if (tw) atomicAdd(&stats[5], tw);
+        if (nsp) atomicAdd(&stats[8], nsp);
+        if (spc) atomicAdd(&stats[9], spc);
+        if (spu) atomicAdd(&stats[10], spu);
+    }
+}
+
 }  // namespace
 
 tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
@@ -436,6 +695,32 @@ tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1,
         reinterpret_cast<unsigned long long *>(d_counts));
     TC_CUDA(cudaGetLastError());
     *launches += 1;
+    return TC_OK;
+}
+
+tc_status upper_plan_device(tc_graph *g, const uint32_t *lo_start, const uint32_t *dD, uint64_t Dub,
+                            unsigned long long *bstats, cudaStream_t s) {
+    const uint64_t ntiles = (Dub + kPlanTile - 1) / kPlanTile;
+    Mem &mem = g->mem;
+    g->plan_items = (BinItemT *)mem.alloc((ntiles ? ntiles : 1) * kPlanTile * sizeof(BinItemT));
+    g->plan_tcount = (uint32_t *)mem.alloc((ntiles ? ntiles : 1) * sizeof(uint32_t));
+    g->plan_big = (uint32_t *)mem.alloc((Dub ? Dub : 1) * sizeof(uint32_t));
+    g->plan_sums = (unsigned long long *)mem.alloc(8 * sizeof(unsigned long long));
+    g->plan_cap_tiles = ntiles ? ntiles : 1;
+    g->plan_cap_big = Dub ? Dub : 1;
+    if (!g->plan_items || !g->plan_tcount || !g->plan_big || !g->plan_sums) {
+        set_error("device allocation for the graph's census plan failed");
+        return TC_E_OOM;
+    }
+    TC_CUDA(cudaMemsetAsync(g->plan_sums, 0, 8 * sizeof(unsigned long long), s));
+    if (ntiles) {
+        const UpperIn I{g->off, g->ups, lo_start, g->dyad_u, g->dyad_e, g->dyad_pb, dD,
+                        g->adj, g->dyad_c, g->dyad_t, g->st.n};
+        k_upper_plan<<<(unsigned)ntiles, kPlanThreads, 0, s>>>(I, g->plan_items, g->plan_tcount,
+                                                              g->plan_big, g->plan_sums, bstats);
+        TC_CUDA(cudaGetLastError());
+        g->launches += 1;
+    }
     return TC_OK;
 }
 
@@ -466,14 +751,30 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     DevBuf<BinItemT> tl;
     DevBuf<BinItemW> wl;
     DevBuf<unsigned long long> stats;
-    if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
-    if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
+    const bool use_graph_plan = g->plan_items && k0 == 0 && k1 == D && !mode64;
+    if (!use_graph_plan) {
+        if ((st = tcount.allocate(mem, ntiles)) != TC_OK) return st;
+        if ((st = tl.allocate(mem, ntiles * kPlanTile)) != TC_OK) return st;
+    }
     if ((st = wl.allocate(mem, wcap)) != TC_OK) return st;
     if ((st = stats.allocate(mem, 11)) != TC_OK) return st;
     TC_CUDA(cudaMemsetAsync(stats.p, 0, 11 * sizeof(unsigned long long), s));
     const PlanIn P{g->dyad_u + k0, g->dyad_e + k0, g->dyad_c + k0, g->dyad_t + k0,
                    g->dyad_pb + k0, g->ups, g->off, g->tagpre != nullptr};
-    if (P.sparse && !mode64)
+    // the whole range in 16-class mode: the graph's own plan (k_upper_plan)
+    const bool resident = g->plan_items && k0 == 0 && k1 == D && !mode64;
+    if (resident) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, g->device);
+        if (P.sparse)
+            k_emit_big<true><<<(unsigned)sms * 8, 256, 0, s>>>(
+                P, g->plan_big, g->plan_sums, wl.p, stats.p,
+                reinterpret_cast<unsigned long long *>(d_counts));
+        else
+            k_emit_big<false><<<(unsigned)sms * 8, 256, 0, s>>>(
+                P, g->plan_big, g->plan_sums, wl.p, stats.p,
+                reinterpret_cast<unsigned long long *>(d_counts));
+    } else if (P.sparse && !mode64)
         k_plan_tile<true><<<(unsigned)ntiles, kPlanThreads, 0, s>>>(
         P, N, g->st.n, tl.p, tcount.p, wl.p, stats.p,
         reinterpret_cast<unsigned long long *>(d_counts), mode64);
@@ -484,8 +785,8 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     TC_CUDA(cudaGetLastError());
     *launches += 1;
     BinLists lists;
-    lists.t = tl.p;
-    lists.t_count = tcount.p;
+    lists.t = resident ? g->plan_items : tl.p;
+    lists.t_count = resident ? g->plan_tcount : tcount.p;
     lists.ntiles = ntiles;
     lists.w = wl.p;
     lists.w_count = stats.p;

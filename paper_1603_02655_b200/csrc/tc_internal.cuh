@@ -92,6 +92,7 @@ constexpr uint32_t kSparseChunk = 256;
 constexpr uint64_t kShardKappa = 8;
 constexpr int kMaxWorld = 1024;   // ranks a shard cut supports
 
+constexpr uint64_t kPlanTileItems = 4096;   // = kPlanTile (census.cuh)
 struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, t = merge length
     uint32_t pa, pb, e, t;   // | (length of the A part) << 16 (both <= 254)
 };
@@ -120,6 +121,16 @@ struct tc_graph {
     // kSparseMinDegree): the skewed-pair path of the warp bin counts the tags
     // of a row range with two loads instead of a merge (census.cu)
     uint64_t *tagpre = nullptr; size_t tagpre_n = 0;
+    size_t adj_alloc_n = 0;             // entries allocated for adj (>= adj_n)
+    // the full-census plan built with the graph (schedule.cu k_upper_plan):
+    // thread-bin items per tile of kPlanTile dyads sorted by merge length, the
+    // tiles' item counts, the big dyads (t > kThreadBinMax) and the sums
+    // [n - c of pre 1..3, thread-bin sum c, thread-bin sum t, big dyads]
+    tc::BinItemT *plan_items = nullptr;
+    uint32_t *plan_tcount = nullptr;
+    uint32_t *plan_big = nullptr;
+    unsigned long long *plan_sums = nullptr;
+    uint64_t plan_cap_tiles = 0, plan_cap_big = 0;
     int profile = 0;
     // results of the most recent build / census call: written once at the
     // end of a call from that call's own locals, under `mu` (a graph may be
@@ -144,6 +155,9 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
 // paper's per-dyad attribution n - |S| - 2 (schedule.cu k_range_dyadic)
 tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
                                     uint64_t *d_counts, tc_profile *prof, uint64_t *launches);
+// a1 + a2 fused: upper row entries, c, t and the graph's full-census plan
+tc_status upper_plan_device(tc_graph *g, const uint32_t *lo_start, const uint32_t *dD, uint64_t Dub,
+                            unsigned long long *bstats, cudaStream_t s);   // schedule.cu
 tc_status shard_bounds_device(const tc_graph *g, int world, cudaStream_t s, uint64_t kappa,
                               uint64_t *bounds);                      // schedule.cu
 tc_status task_queues_device(const tc_graph *g, int nonuniform, uint64_t max_nset, cudaStream_t s,
