@@ -551,15 +551,37 @@ __device__ __forceinline__ uint32_t lower_id(const uint32_t *__restrict__ L, uin
     return lo;
 }
 
-__device__ __forceinline__ uint32_t tag_in(const uint32_t *__restrict__ L, uint32_t len,
-                                           uint32_t x) {
-    const uint32_t p = lower_id(L, len, x);
-    if (p < len) {
-        const uint32_t e = __ldg(L + p);
-        if ((e >> 2) == x) return e & 3u;
+// K independent lower_id searches in lockstep (fixed-step branch-free binary
+// search: the same number of probes for every key of the same list), so K
+// dependent-load chains are in flight per lane instead of one (the skewed
+// path is bound by the probes' L2 latency)
+template <int K>
+__device__ __forceinline__ void tag_in_k(const uint32_t *__restrict__ L, uint32_t len,
+                                         const uint32_t (&x)[K], uint32_t (&tag)[K]) {
+    uint32_t lo[K];
+#pragma unroll
+    for (int q = 0; q < K; q++) lo[q] = 0;
+    uint32_t step = len ? 1u << (31 - __clz(len)) : 0u;
+    for (; step; step >>= 1) {
+#pragma unroll
+        for (int q = 0; q < K; q++) {
+            const uint32_t p = lo[q] + step;
+            if (p <= len && (__ldg(L + p - 1) >> 2) < x[q]) lo[q] = p;
+        }
     }
-    return 0u;
+#pragma unroll
+    for (int q = 0; q < K; q++) {
+        tag[q] = 0u;
+        if (lo[q] < len) {
+            const uint32_t e = __ldg(L + lo[q]);
+            if ((e >> 2) == x[q]) tag[q] = e & 3u;
+        }
+    }
 }
+
+#ifndef TC_SP_K
+#define TC_SP_K 2
+#endif
 
 // skewed-pair class counts: per-warp uint32 shared counters (native 32-bit
 // shared atomics; 64-bit shared atomics are CAS loops on sm_100), added
@@ -603,19 +625,30 @@ __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__
     const uint32_t v = w.e >> 2, pre = w.e & 3u;
     const uint32_t minus1 = ~0u;
     uint32_t own = 0, o012 = 0, o102 = 0;
+    constexpr int K = TC_SP_K;
     if (mode == 1u) {
-        for (uint32_t j = d0 + lane; j < d1; j += 32) {
-            const uint32_t x = __ldg(adj + w.oa + j), id = x >> 2, tu = x & 3u;
-            if (id == v) continue;
-            const uint32_t tv = tag_in(adj + w.ob, w.b, id);
-            if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
-            if (tv) {
-                own++;
-                if (id > v) {
-                    o102 += tv == 3u;
-                    o012 += tv != 3u;
+        for (uint32_t j0 = d0 + lane; j0 < d1; j0 += 32 * K) {
+            uint32_t xs[K], ids[K], tvs[K];
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const uint32_t j = j0 + 32 * q;
+                xs[q] = j < d1 ? __ldg(adj + w.oa + j) : 0xffffffffu;
+                ids[q] = xs[q] >> 2;
+            }
+            tag_in_k<K>(adj + w.ob, w.b, ids, tvs);
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const uint32_t id = ids[q], tu = xs[q] & 3u, tv = tvs[q];
+                if (j0 + 32 * q >= d1 || id == v) continue;
+                if (id > v) sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
+                if (tv) {
+                    own++;
+                    if (id > v) {
+                        o102 += tv == 3u;
+                        o012 += tv != 3u;
+                    }
+                    sp_add(sp, c_triad_table[pre | tv << 4], minus1);
                 }
-                sp_add(sp, c_triad_table[pre | tv << 4], minus1);
             }
         }
         if (d0 == 0 && lane == 0) {
@@ -626,18 +659,29 @@ __device__ void sparse_item(const uint32_t *__restrict__ adj, const uint64_t *__
                 if (cnt[t]) sp_add(sp, c_triad_table[pre | t << 4], cnt[t]);
         }
     } else {
-        for (uint32_t j = d0 + lane; j < d1; j += 32) {
-            const uint32_t y = __ldg(adj + w.ob + j), id = y >> 2, tv = y & 3u;
-            const uint32_t tu = tag_in(adj + w.oa, w.a, id);
-            if (!tu) {
-                sp_add(sp, c_triad_table[pre | tv << 4], 1u);
-            } else {
-                own++;
-                if (id > v) {
-                    sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
-                    o102 += tv == 3u;
-                    o012 += tv != 3u;
-                    sp_add(sp, c_triad_table[pre | tu << 2], minus1);
+        for (uint32_t j0 = d0 + lane; j0 < d1; j0 += 32 * K) {
+            uint32_t ys[K], ids[K], tus[K];
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const uint32_t j = j0 + 32 * q;
+                ys[q] = j < d1 ? __ldg(adj + w.ob + j) : 0xffffffffu;
+                ids[q] = ys[q] >> 2;
+            }
+            tag_in_k<K>(adj + w.oa, w.a, ids, tus);
+#pragma unroll
+            for (int q = 0; q < K; q++) {
+                const uint32_t id = ids[q], tv = ys[q] & 3u, tu = tus[q];
+                if (j0 + 32 * q >= d1) continue;
+                if (!tu) {
+                    sp_add(sp, c_triad_table[pre | tv << 4], 1u);
+                } else {
+                    own++;
+                    if (id > v) {
+                        sp_add(sp, c_triad_table[pre | tu << 2 | tv << 4], 1u);
+                        o102 += tv == 3u;
+                        o012 += tv != 3u;
+                        sp_add(sp, c_triad_table[pre | tu << 2], minus1);
+                    }
                 }
             }
         }
