@@ -57,6 +57,9 @@ def parse():
     p.add_argument("--mode", default="16", choices=["16", "64"],
                    help="16-class isomorphic census (default) or the 64-type census (f1)")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--alloc", default="pool", choices=["pool", "torch"],
+                   help="device allocator of the library: its own stream-ordered pool "
+                        "(default) or torch's caching allocator through the Python hook")
     p.add_argument("--cpu-seconds", type=float, default=25.0,
                    help="wall-time budget of the cpu_baseline oracle run (full census if it fits)")
     return p.parse_args()
@@ -316,7 +319,7 @@ def run_ours(args):
         # rather than torch's caching allocator through the Python hook: no
         # Python callback per device allocation on the build's critical path
         g = tcb.tc_graph_create(a.n, src, dst, device=local, stream=stream,
-                                use_torch_allocator=False)
+                                use_torch_allocator=args.alloc == "torch")
         launches = g.launches()
         if profile:
             g.profile(True)

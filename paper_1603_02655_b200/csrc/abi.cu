@@ -7,6 +7,8 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -45,14 +47,61 @@ static void keep_default_pool() {
     done_dev = dev;
 }
 
+// Exact-size block cache in front of the pool: a freed block is kept under
+// (device, stream, bytes) and handed to the next request of the same size on
+// the same stream (stream order makes the reuse safe without a sync), so the
+// repeated builds and censuses of one graph size allocate nothing from the
+// driver after the first.  Measured: with cudaMallocAsync alone, C4's build
+// and plan swung between 15 and 600 ms per step (pool growth on the large
+// requests); with the cache they are as steady as torch's caching allocator.
+// Blocks beyond kCacheCap bytes go back to the pool.
+namespace {
+struct BlockKey {
+    int dev;
+    cudaStream_t stream;
+    size_t bytes;
+    bool operator<(const BlockKey &o) const {
+        if (dev != o.dev) return dev < o.dev;
+        if (stream != o.stream) return stream < o.stream;
+        return bytes < o.bytes;
+    }
+};
+std::mutex g_cache_mu;
+std::map<BlockKey, std::vector<void *>> g_cache;
+size_t g_cached = 0;
+constexpr size_t kCacheCap = 64ull << 30;
+}  // namespace
+
 void *Mem::alloc(size_t bytes) {
     if (bytes == 0) bytes = 1;
     if (custom) return hook.alloc(bytes, (void *)stream, hook.ctx);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        auto it = g_cache.find(BlockKey{dev, stream, bytes});
+        if (it != g_cache.end() && !it->second.empty()) {
+            void *p = it->second.back();
+            it->second.pop_back();
+            g_cached -= bytes;
+            return p;
+        }
+    }
     keep_default_pool();
     void *p = nullptr;
     if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
         cudaGetLastError();
-        return nullptr;
+        // give the cached blocks back to the pool and retry once
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (auto &kv : g_cache)
+            for (void *q : kv.second) cudaFreeAsync(q, kv.first.stream);
+        g_cache.clear();
+        g_cached = 0;
+        cudaDeviceSynchronize();
+        if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
     }
     return p;
 }
@@ -60,8 +109,21 @@ void *Mem::alloc(size_t bytes) {
 void Mem::free(void *p, size_t bytes) {
     if (!p) return;
     if (bytes == 0) bytes = 1;
-    if (custom) hook.free(p, bytes, (void *)stream, hook.ctx);
-    else cudaFreeAsync(p, stream);
+    if (custom) {
+        hook.free(p, bytes, (void *)stream, hook.ctx);
+        return;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        if (g_cached + bytes <= kCacheCap) {
+            g_cache[BlockKey{dev, stream, bytes}].push_back(p);
+            g_cached += bytes;
+            return;
+        }
+    }
+    cudaFreeAsync(p, stream);
 }
 
 // ---- 128-bit closing (a5) ------------------------------------------------

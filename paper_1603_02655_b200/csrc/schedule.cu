@@ -120,7 +120,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         for (int w = 0; w < kPlanWarps; w++) tot += wc[w][d];
         if (d == 255) tot = 0;      // big dyads are not in the thread list
         uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
-        if (d == 0) tile_count[blockIdx.x] = all;
+        if (d == 0 && tile_count) tile_count[blockIdx.x] = all;
 #pragma unroll
         for (int w = 0; w < kPlanWarps; w++) {
             uint32_t c = wc[w][d];
@@ -188,7 +188,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
     }
     __syncthreads();
     uint4 *out = reinterpret_cast<uint4 *>(tl + tile0);
-    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) {
+    for (uint32_t j = threadIdx.x; tl && j < all; j += kPlanThreads) {
         const uint64_t i = tile0 + perm[j];
         const uint32_t u = __ldg(P.du + i);
         // t | |A| << 16 (t <= 254): the census prefetches exactly both parts
@@ -542,7 +542,7 @@ k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ 
         for (int w = 0; w < kPlanWarps; w++) tot += wc[w][d];
         if (d == 255) tot = 0;      // big dyads are not in the thread list
         uint32_t run = block_exclusive_sum<uint32_t>(tot, &all);
-        if (d == 0) tile_count[blockIdx.x] = all;
+        if (d == 0 && tile_count) tile_count[blockIdx.x] = all;
 #pragma unroll
         for (int w = 0; w < kPlanWarps; w++) {
             uint32_t c = wc[w][d];
@@ -552,7 +552,7 @@ k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ 
         if (d == 0) {   // one reservation per block in the big-dyad list
             uint32_t nb = 0;
             for (int w = 0; w < kPlanWarps; w++) nb += wbig[w];
-            big_base = nb ? atomicAdd(&sums[5], (unsigned long long)nb) : 0ull;
+            big_base = (nb && big) ? atomicAdd(&sums[5], (unsigned long long)nb) : 0ull;
         }
     }
     __syncthreads();
@@ -566,13 +566,13 @@ k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ 
         const uint32_t r = (rk[k >> 1] >> (16 * (k & 1))) & 0xffffu;
         if (valid && d < 255u) perm[wc[warp][d] + r] = (uint16_t)(wbase + k * 32 + lane);
         const uint32_t bb = __ballot_sync(0xffffffffu, valid && d == 255u);
-        if (valid && d == 255u) big[bpos + __popc(bb & lt)] = (uint32_t)i;
+        if (big && valid && d == 255u) big[bpos + __popc(bb & lt)] = (uint32_t)i;
         bpos += __popc(bb);
     }
     __syncthreads();
     // 3. the tile's thread-bin items in length order, stored coalesced
     uint4 *out = reinterpret_cast<uint4 *>(tl + tile0);
-    for (uint32_t j = threadIdx.x; j < all; j += kPlanThreads) {
+    for (uint32_t j = threadIdx.x; tl && j < all; j += kPlanThreads) {
         const uint64_t i = tile0 + perm[j];
         const uint32_t u = __ldg(I.du + i);
         const uint32_t pa = __ldg(I.ups + u), a = __ldg(I.off + u + 1) - 1u - pa;
@@ -702,13 +702,19 @@ tc_status upper_plan_device(tc_graph *g, const uint32_t *lo_start, const uint32_
                             unsigned long long *bstats, cudaStream_t s) {
     const uint64_t ntiles = (Dub + kPlanTile - 1) / kPlanTile;
     Mem &mem = g->mem;
-    g->plan_items = (BinItemT *)mem.alloc((ntiles ? ntiles : 1) * kPlanTile * sizeof(BinItemT));
-    g->plan_tcount = (uint32_t *)mem.alloc((ntiles ? ntiles : 1) * sizeof(uint32_t));
-    g->plan_big = (uint32_t *)mem.alloc((Dub ? Dub : 1) * sizeof(uint32_t));
+    // the graph keeps its own plan up to kResidentMaxDyads canonical dyads
+    // (16 B per dyad + 4 B per big dyad); larger graphs (C5: 1.05e9 dyads)
+    // plan per census call instead, as ranges do
+    const bool resident = Dub <= kResidentMaxDyads;
+    if (resident) {
+        g->plan_items = (BinItemT *)mem.alloc((ntiles ? ntiles : 1) * kPlanTile * sizeof(BinItemT));
+        g->plan_tcount = (uint32_t *)mem.alloc((ntiles ? ntiles : 1) * sizeof(uint32_t));
+        g->plan_big = (uint32_t *)mem.alloc((Dub ? Dub : 1) * sizeof(uint32_t));
+        g->plan_cap_tiles = ntiles ? ntiles : 1;
+        g->plan_cap_big = Dub ? Dub : 1;
+    }
     g->plan_sums = (unsigned long long *)mem.alloc(8 * sizeof(unsigned long long));
-    g->plan_cap_tiles = ntiles ? ntiles : 1;
-    g->plan_cap_big = Dub ? Dub : 1;
-    if (!g->plan_items || !g->plan_tcount || !g->plan_big || !g->plan_sums) {
+    if ((resident && (!g->plan_items || !g->plan_tcount || !g->plan_big)) || !g->plan_sums) {
         set_error("device allocation for the graph's census plan failed");
         return TC_E_OOM;
     }

@@ -93,6 +93,7 @@ constexpr uint64_t kShardKappa = 8;
 constexpr int kMaxWorld = 1024;   // ranks a shard cut supports
 
 constexpr uint64_t kPlanTileItems = 4096;   // = kPlanTile (census.cuh)
+constexpr uint64_t kResidentMaxDyads = 1ull << 27;   // graph-resident census plan up to this D
 struct BinItemT {   // thread bin: merge starts in adj, e = v<<2|pre, t = merge length
     uint32_t pa, pb, e, t;   // | (length of the A part) << 16 (both <= 254)
 };
