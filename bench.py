@@ -299,6 +299,10 @@ def run_ours(args):
         n_, s_dev, d_dev, meta_ = make_device_config(args.config, dev)
         a = synth.Arcs(n_, None, None, meta_)
         a_m = int(s_dev.numel())
+        # the draw's temporaries stay in torch's cache otherwise; the library
+        # allocates from its own pool (C5 needs ~130 GB of it)
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
     else:
         a = synth.make_config(args.config)
         a_m = a.m

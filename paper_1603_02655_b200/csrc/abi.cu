@@ -54,7 +54,8 @@ static void keep_default_pool() {
 // driver after the first.  Measured: with cudaMallocAsync alone, C4's build
 // and plan swung between 15 and 600 ms per step (pool growth on the large
 // requests); with the cache they are as steady as torch's caching allocator.
-// Blocks beyond kCacheCap bytes go back to the pool.
+// Blocks beyond kCacheCap bytes in total, or above kCacheMaxBlock each, go
+// back to the pool.
 namespace {
 struct BlockKey {
     int dev;
@@ -69,7 +70,8 @@ struct BlockKey {
 std::mutex g_cache_mu;
 std::map<BlockKey, std::vector<void *>> g_cache;
 size_t g_cached = 0;
-constexpr size_t kCacheCap = 64ull << 30;
+constexpr size_t kCacheCap = 120ull << 30;
+constexpr size_t kCacheMaxBlock = 80ull << 30;
 }  // namespace
 
 void *Mem::alloc(size_t bytes) {
@@ -91,13 +93,17 @@ void *Mem::alloc(size_t bytes) {
     void *p = nullptr;
     if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
         cudaGetLastError();
-        // give the cached blocks back to the pool and retry once
+        // give the cached blocks back to the pool, the pool's unused
+        // reservations back to the driver, and retry once (a request larger
+        // than any free chunk needs fresh physical memory)
         std::lock_guard<std::mutex> lk(g_cache_mu);
         for (auto &kv : g_cache)
             for (void *q : kv.second) cudaFreeAsync(q, kv.first.stream);
         g_cache.clear();
         g_cached = 0;
         cudaDeviceSynchronize();
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
         if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
             cudaGetLastError();
             return nullptr;
@@ -117,7 +123,7 @@ void Mem::free(void *p, size_t bytes) {
     cudaGetDevice(&dev);
     {
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        if (g_cached + bytes <= kCacheCap) {
+        if (bytes <= kCacheMaxBlock && g_cached + bytes <= kCacheCap) {
             g_cache[BlockKey{dev, stream, bytes}].push_back(p);
             g_cached += bytes;
             return;
