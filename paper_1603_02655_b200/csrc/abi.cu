@@ -138,6 +138,62 @@ static unsigned __int128 choose3(uint64_t n) {
     return (unsigned __int128)n * (n - 1) * (n - 2) / 6;
 }
 
+// pinned host slots for the lazy end of the build (16 words each), allocated
+// once per process on first use
+namespace {
+std::mutex g_pin_mu;
+unsigned long long *g_pin_base = nullptr;
+std::vector<int> g_pin_free;
+constexpr int kPinSlots = 1024, kPinWords = 16;
+
+int pin_acquire(unsigned long long **p) {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_base) {
+        void *q = nullptr;
+        if (cudaMallocHost(&q, (size_t)kPinSlots * kPinWords * 8) != cudaSuccess) {
+            cudaGetLastError();
+            return -1;
+        }
+        g_pin_base = (unsigned long long *)q;
+        for (int i = kPinSlots - 1; i >= 0; i--) g_pin_free.push_back(i);
+    }
+    if (g_pin_free.empty()) return -1;
+    const int slot = g_pin_free.back();
+    g_pin_free.pop_back();
+    *p = g_pin_base + (size_t)slot * kPinWords;
+    return slot;
+}
+
+void pin_release(int slot) {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back(slot);
+}
+}  // namespace
+
+tc_status graph_finalize(const tc_graph *gc) {
+    tc_graph *g = const_cast<tc_graph *>(gc);
+    if (g->final_.load()) return TC_OK;
+    std::lock_guard<std::mutex> lk(g->mu);
+    if (g->final_.load()) return TC_OK;
+    TC_CUDA(cudaSetDevice(g->device));
+    TC_CUDA(cudaEventSynchronize(g->ready));
+    if (g->ev_b0) {
+        cudaEventElapsedTime(&g->prof.build_ms, g->ev_b0, g->ev_b1);
+        cudaEventDestroy(g->ev_b0);
+        cudaEventDestroy(g->ev_b1);
+        g->ev_b0 = g->ev_b1 = nullptr;
+    }
+    const tc_status st = build_finish(g, g->pin, (uint32_t)g->pin[8]);
+    cudaEventDestroy(g->ready);
+    g->ready = nullptr;
+    pin_release(g->pin_slot);
+    g->pin_slot = -1;
+    g->pin = nullptr;
+    g->final_ = true;
+    return st;
+}
+
 }  // namespace tc
 
 using namespace tc;
@@ -227,13 +283,32 @@ tc_status tc_graph_create(int device, uint64_t n, const uint32_t *src, const uin
     }
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
+    // lazy end of the build (graph_finalize) when a pinned slot is free
+    g->pin_slot = pin_acquire(&g->pin);
+    if (g->pin_slot >= 0 && cudaEventCreateWithFlags(&g->ready, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        pin_release(g->pin_slot);
+        g->pin_slot = -1;
+        g->pin = nullptr;
+    }
     cudaEventRecord(e0, s);
     st = build_csr(g, ds, dd, m, s);
     cudaEventRecord(e1, s);
-    if (cudaEventSynchronize(e1) == cudaSuccess)
-        cudaEventElapsedTime(&g->prof.build_ms, e0, e1);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
+    if (st == TC_OK && !g->final_.load()) {   // finalized by the first query
+        g->ev_b0 = e0;
+        g->ev_b1 = e1;
+    } else {
+        if (cudaEventSynchronize(e1) == cudaSuccess)
+            cudaEventElapsedTime(&g->prof.build_ms, e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        if (g->ready) cudaEventDestroy(g->ready);
+        g->ready = nullptr;
+        pin_release(g->pin_slot);
+        g->pin_slot = -1;
+        g->pin = nullptr;
+        g->final_ = true;
+    }
     hs.release();
     hd.release();
     if (st != TC_OK) {
@@ -251,6 +326,7 @@ tc_status tc_graph_stats_get(const tc_graph *g, tc_graph_stats *out) {
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     *out = g->st;
     return TC_OK;
 }
@@ -258,6 +334,14 @@ tc_status tc_graph_stats_get(const tc_graph *g, tc_graph_stats *out) {
 void tc_graph_destroy(tc_graph *g) {
     if (!g) return;
     cudaSetDevice(g->device);
+    if (!g->final_.load()) {   // a graph destroyed before any query
+        cudaEventSynchronize(g->ready);
+        if (g->ev_b0) cudaEventDestroy(g->ev_b0);
+        if (g->ev_b1) cudaEventDestroy(g->ev_b1);
+        cudaEventDestroy(g->ready);
+        pin_release(g->pin_slot);
+        g->final_ = true;
+    }
     g->mem.free(g->off, g->off_n * 4);
     g->mem.free(g->adj, (g->adj_alloc_n ? g->adj_alloc_n : g->adj_n) * 4);
     g->mem.free(g->dyad_u, g->dyad_n * 4);
@@ -289,6 +373,7 @@ tc_status tc_profile_get(const tc_graph *g, tc_profile *out) {
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
     return TC_OK;
@@ -325,6 +410,7 @@ tc_status tc_census_enqueue(const tc_graph *g, uint64_t dyad_begin, uint64_t dya
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     TC_CUDA(cudaSetDevice(g->device));
     CallRec r;
     const tc_status st = census_range_device(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream,
@@ -361,6 +447,7 @@ tc_status tc_census(const tc_graph *g, void *cuda_stream, uint64_t counts[16], u
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     tc_status st = census_partial_sync(g, 0, g->st.dyads, (cudaStream_t)cuda_stream, counts, 0);
     if (st != TC_OK) return st;
     return tc_close_census(g->st.n, counts, c003_hi);
@@ -372,6 +459,7 @@ tc_status tc_census_range(const tc_graph *g, uint64_t dyad_begin, uint64_t dyad_
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     return census_partial_sync(g, dyad_begin, dyad_end, (cudaStream_t)cuda_stream, partial, 1);
 }
 
@@ -381,6 +469,7 @@ tc_status tc_census64(const tc_graph *g, void *cuda_stream, uint64_t counts[64],
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     TC_CUDA(cudaSetDevice(g->device));
     cudaStream_t s = (cudaStream_t)cuda_stream;
     Mem mem = g->mem;
@@ -446,6 +535,7 @@ tc_status tc_task_queues(const tc_graph *g, int strategy, uint64_t max_nset_size
         set_error("invalid task-queue arguments");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     TC_CUDA(cudaSetDevice(g->device));
     return task_queues_device(g, strategy == TC_QUEUES_NONUNIFORM, max_nset_size,
                               (cudaStream_t)cuda_stream, starts, cap, nqueues, total_nset);
@@ -456,6 +546,7 @@ tc_status tc_shard_bounds(const tc_graph *g, int world, void *cuda_stream, uint6
         set_error("invalid shard arguments");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     TC_CUDA(cudaSetDevice(g->device));
     return shard_bounds_device(g, world, (cudaStream_t)cuda_stream, kShardKappa, bounds);
 }
@@ -612,6 +703,7 @@ tc_status tc_census_multi(const tc_graph *g, tc_comm *comm, void *cuda_stream,
         set_error("NULL argument");
         return TC_E_INVALID;
     }
+    if (tc_status fs = graph_finalize(g)) return fs;
     Nccl *n = nccl();
     if (!n) {
         set_error("libnccl.so.2 could not be loaded");

@@ -860,14 +860,30 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     if ((st = upper_plan_device(g, lo_start.p, total.p, Dub, scratch.p + 4, s)) != TC_OK)
         return st;
     TC_CUDA(cudaGetLastError());
+    g->st.m_in = m;
+    if (g->pin) {   // lazy end: the stats land in the graph's pinned slot
+        TC_CUDA(cudaMemcpyAsync(g->pin, scratch.p, 8 * sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaMemcpyAsync(g->pin + 8, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+        TC_CUDA(cudaEventRecord(g->ready, s));
+        g->final_ = false;
+        return TC_OK;
+    }
     TC_CUDA(cudaMemcpyAsync(h, scratch.p, sizeof(h), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaMemcpyAsync(&D, total.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
     TC_CUDA(cudaStreamSynchronize(s));
+    return build_finish(g, h, D);
+}
+
+tc_status build_finish(tc_graph *g, const unsigned long long *h, uint32_t D) {
+    const uint64_t n = g->st.n, m = g->st.m_in;
     const uint64_t loops = h[1];
     const uint64_t nnz = 2ull * D;
     g->adj_n = nnz + n + 8;
     // 7. tag prefix counts for the skewed-pair path (hub graphs only)
     if (h[5] >= kSparseMinDegree) {
+        Mem &mem = g->mem;
+        cudaStream_t s = g->stream;
         const size_t nt = nnz + n + 8;
         uint64_t *tp = (uint64_t *)mem.alloc((nt + 1) * sizeof(uint64_t));
         if (!tp) {
@@ -876,12 +892,12 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         }
         g->tagpre = tp;
         g->tagpre_n = nt + 1;
-        if ((st = scan_exclusive<uint64_t>(mem, nt, TagIn{adj}, ArrayOutExcl<uint64_t>{tp},
+        tc_status st;
+        if ((st = scan_exclusive<uint64_t>(mem, nt, TagIn{g->adj}, ArrayOutExcl<uint64_t>{tp},
                                            tp + nt, s, &g->launches)) != TC_OK)
             return st;
         TC_CUDA(cudaStreamSynchronize(s));
     }
-    g->st.m_in = m;
     g->st.loops_dropped = loops;
     g->st.dyads = D;
     g->st.sum_deg_sq = h[4];

@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -123,6 +124,14 @@ struct tc_graph {
     // of a row range with two loads instead of a merge (census.cu)
     uint64_t *tagpre = nullptr; size_t tagpre_n = 0;
     size_t adj_alloc_n = 0;             // entries allocated for adj (>= adj_n)
+    // lazy end of the build: the stats and D are copied into a pinned slot
+    // and `ready` is recorded; the first call that needs the host-side stats
+    // waits there (graph_finalize), so the caller's own host work between
+    // tc_graph_create and the census overlaps the build's last kernels
+    unsigned long long *pin = nullptr;
+    int pin_slot = -1;
+    cudaEvent_t ready = nullptr, ev_b0 = nullptr, ev_b1 = nullptr;
+    std::atomic<bool> final_{true};
     // the full-census plan built with the graph (schedule.cu k_upper_plan):
     // thread-bin items per tile of kPlanTile dyads sorted by merge length, the
     // tiles' item counts, the big dyads (t > kThreadBinMax) and the sums
@@ -156,6 +165,12 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
 // paper's per-dyad attribution n - |S| - 2 (schedule.cu k_range_dyadic)
 tc_status census_range_paper_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaStream_t s,
                                     uint64_t *d_counts, tc_profile *prof, uint64_t *launches);
+// the host side of the build's end (stats, adjacency size, the tag prefix
+// of hub graphs) from the values the device wrote: h[8] stats, D (csr_build.cu)
+tc_status build_finish(tc_graph *g, const unsigned long long *h, uint32_t D);
+// waits for a lazily ended build and runs build_finish once (abi.cu); every
+// entry point that reads the graph's host-side stats calls it first
+tc_status graph_finalize(const tc_graph *g);
 // a1 + a2 fused: upper row entries, c, t and the graph's full-census plan
 tc_status upper_plan_device(tc_graph *g, const uint32_t *lo_start, const uint32_t *dD, uint64_t Dub,
                             unsigned long long *bstats, cudaStream_t s);   // schedule.cu
