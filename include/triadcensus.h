@@ -34,9 +34,14 @@
  *    error, tc_last_error() gives a message (thread-local, valid until the
  *    next call on that thread).
  *  - Device work is issued on the caller's CUDA stream (cudaStream_t passed
- *    as void*; NULL = legacy default stream).  tc_graph_create, tc_census,
- *    tc_census_range and tc_census_multi return after the stream has drained
- *    (results on the host); tc_census_enqueue does not synchronise.
+ *    as void*; NULL = legacy default stream).  tc_census, tc_census_range
+ *    and tc_census_multi return after the stream has drained (results on the
+ *    host); tc_census_enqueue does not synchronise.  tc_graph_create returns
+ *    once the build is enqueued (arc range errors are reported by it, after
+ *    a mid-build host read); the graph's statistics reach the host at the
+ *    first call that needs them (stats, profile, any census, shard or queue
+ *    call), which waits for the build to finish.  Host arc arrays may be
+ *    reused as soon as tc_graph_create returns (they are copied first).
  *  - A tc_graph may be shared read-only by concurrent census calls on
  *    different streams (and host threads): a call keeps its launch count
  *    and profile in its own locals and publishes them to the graph's
