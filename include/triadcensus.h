@@ -102,7 +102,9 @@ typedef struct {
     float build_ms;         /* a1: sort + dedup + symmetrise + offsets + stats */
     float plan_ms;          /* a2: per-dyad cost and degree bins */
     float census_ms;        /* a3+a4: all bin kernels incl. histogram flush */
-    float kernel_ms[4];     /* a3+a4 per bin: [0] thread bin, [1] warp bin, [2..3] 0 */
+    float kernel_ms[4];     /* a3+a4 per bin: [0] thread bin, [1] warp bin (it runs on a
+                               side stream beside the thread bin: from the bins' start
+                               to its end), [2..3] 0 */
     uint64_t bin_items[4];  /* [0] thread-bin dyads, [1] warp items, [2] warp-bin dyads,
                                [3] of those, skewed-pair dyads (searched, not merged) */
     uint64_t bin_work[4];   /* [0] / [1] thread / warp bin: sum of |N(u)|+|N(v)| (the

@@ -898,12 +898,14 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     // once per device (host time between the plan and the bins is exposed)
     struct Occ {
         int sms, thread, warp, thread64, warp64;
+        cudaStream_t side;   // the warp bin runs here, beside the thread bin
     };
     static Occ occ[64];
     static std::atomic<uint64_t> occ_done{0};
     const int dv = g->device & 63;
     if (!(occ_done.load() & (1ull << dv))) {
-        Occ o{148, 0, 0, 0, 0};
+        Occ o{148, 0, 0, 0, 0, nullptr};
+        TC_CUDA(cudaStreamCreateWithFlags(&o.side, cudaStreamNonBlocking));
         cudaDeviceGetAttribute(&o.sms, cudaDevAttrMultiProcessorCount, g->device);
         TC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.warp64, k_census_warp64,
                                                               kCensusThreads, 0));
@@ -926,7 +928,21 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     const uint32_t upt = bl.ntiles >= 4 * tgrid ? 2u : 4u;   // units per plan tile
     const uint64_t units = bl.ntiles * upt;
     if (tgrid > units) tgrid = units ? units : 1;
-    if (ev) TC_CUDA(cudaEventRecord(ev[0], s));
+    // the two bins are independent (own item lists and cursors, atomic adds
+    // into the census): the warp bin runs on a side stream, so it fills the
+    // SMs the thread bin's tail leaves idle (and the reverse at C2/C4/C5).
+    // ev (profiling): [0] start, [1] thread bin done, [2] both done (on s),
+    // [3] warp bin done (on the side stream)
+    const cudaStream_t side = occ[dv].side;
+    cudaEvent_t fork = nullptr, join = nullptr;
+    TC_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    if (ev) {
+        fork = ev[0];
+    } else {
+        TC_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    }
+    TC_CUDA(cudaEventRecord(fork, s));
+    TC_CUDA(cudaStreamWaitEvent(side, fork, 0));
     if (mode64)
         k_census_thread64<<<(unsigned)tgrid, kCensusThreads, 0, s>>>(bl.t, bl.t_count, bl.ntiles,
                                                                     g->adj, out, bl.cursor, upt);
@@ -936,11 +952,16 @@ tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uin
     TC_CUDA(cudaGetLastError());
     if (ev) TC_CUDA(cudaEventRecord(ev[1], s));
     if (mode64)
-        k_census_warp64<<<grid, kCensusThreads, 0, s>>>(bl, g->off, g->ups, g->adj, out);
+        k_census_warp64<<<grid, kCensusThreads, 0, side>>>(bl, g->off, g->ups, g->adj, out);
     else
-        k_census_warp<<<grid, kCensusThreads, 0, s>>>(bl, g->off, g->ups, g->adj, out);
+        k_census_warp<<<grid, kCensusThreads, 0, side>>>(bl, g->off, g->ups, g->adj, out);
     TC_CUDA(cudaGetLastError());
+    if (ev) TC_CUDA(cudaEventRecord(ev[3], side));
+    TC_CUDA(cudaEventRecord(join, side));
+    TC_CUDA(cudaStreamWaitEvent(s, join, 0));
     if (ev) TC_CUDA(cudaEventRecord(ev[2], s));
+    cudaEventDestroy(join);
+    if (!ev) cudaEventDestroy(fork);
     *launches += 2;
     return TC_OK;
 }

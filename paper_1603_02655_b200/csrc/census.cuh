@@ -28,6 +28,6 @@ static_assert(kPlanTile == kPlanTileItems, "plan tile size");
 // a3 + a4: launches the bin kernels; ADDS classes 2..16 into d_counts[1..15]
 // (mode64: TriadCodes 1..63 into d_counts[1..63])
 tc_status launch_bins(const tc_graph *g, const BinLists &bl, cudaStream_t s, uint64_t *d_counts,
-                      cudaEvent_t *ev /* 3 events or null */, uint64_t *launches, int mode64);
+                      cudaEvent_t *ev /* 4 events or null */, uint64_t *launches, int mode64);
 
 }  // namespace tc

@@ -743,9 +743,9 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
     }
     Mem mem = g->mem;
     mem.stream = s;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     if (prof) {
-        for (int i = 0; i < 4; i++) TC_CUDA(cudaEventCreate(&ev[i]));
+        for (int i = 0; i < 5; i++) TC_CUDA(cudaEventCreate(&ev[i]));
         TC_CUDA(cudaEventRecord(ev[0], s));
     }
     tc_status st;
@@ -815,7 +815,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->plan_ms = t;
         TC_CUDA(cudaEventElapsedTime(&t, ev[1], ev[2]));
         prof->kernel_ms[0] = t;
-        TC_CUDA(cudaEventElapsedTime(&t, ev[2], ev[3]));
+        TC_CUDA(cudaEventElapsedTime(&t, ev[1], ev[4]));   // warp bin, on the side stream
         prof->kernel_ms[1] = t;
         prof->kernel_ms[2] = prof->kernel_ms[3] = 0;
         TC_CUDA(cudaEventElapsedTime(&t, ev[1], ev[3]));
@@ -830,7 +830,7 @@ tc_status census_range_device(const tc_graph *g, uint64_t k0, uint64_t k1, cudaS
         prof->bin_work[3] = hs[5];
         prof->sparse_sum_c = hs[9];
         prof->sparse_units = hs[10];
-        for (int i = 0; i < 4; i++) cudaEventDestroy(ev[i]);
+        for (int i = 0; i < 5; i++) cudaEventDestroy(ev[i]);
     }
     return TC_OK;
 }
