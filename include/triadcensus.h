@@ -75,8 +75,12 @@ typedef enum {
 
 /* Device memory hook.  alloc(bytes, stream, ctx) returns a device pointer
  * usable on `stream` (or NULL on failure); free(ptr, bytes, stream, ctx)
- * releases it.  Pass NULL for the default (cudaMallocAsync/cudaFreeAsync on
- * the call's stream).  The Python binding passes torch's caching allocator. */
+ * releases it.  Pass NULL for the default: cudaMallocAsync on the call's
+ * stream behind an exact-size block cache (a freed block is kept under its
+ * device, stream and size and handed to the next request of that size on
+ * that stream; up to 120 GB per process; tc_trim_memory returns it to the
+ * driver).  The Python binding passes torch's caching allocator unless asked
+ * for the default. */
 typedef struct {
     void *(*alloc)(size_t bytes, void *stream, void *ctx);
     void (*free)(void *ptr, size_t bytes, void *stream, void *ctx);
@@ -283,6 +287,12 @@ uint64_t tc_launch_count(const tc_graph *g);
 tc_status tc_read_arcs(const char *path, int format, int index_base, uint64_t *n, uint32_t **src,
                        uint32_t **dst, uint64_t *m);
 void tc_free_arcs(uint32_t *p);
+
+/* Return the default allocator's cached device blocks (all devices) and the
+ * pools' unused reservations to the driver; waits for every device to go
+ * idle.  Call it before destroying a stream whose graphs or census calls
+ * used the default allocator, or to give memory back to other libraries. */
+tc_status tc_trim_memory(void);
 
 const char *tc_last_error(void);
 int tc_abi_version(void);

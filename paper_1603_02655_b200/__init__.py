@@ -299,6 +299,12 @@ def tc_census_multi(g: Graph, comm: Comm, stream=None) -> list[int]:
     return _join003(c, hi.value)
 
 
+def tc_trim_memory() -> None:
+    """Give the default allocator's cached device blocks back to the driver
+    (include/triadcensus.h tc_trim_memory)."""
+    check(lib.tc_trim_memory(), "tc_trim_memory")
+
+
 def census(n: int, src, dst, device: int = 0) -> list[int]:
     """One-shot: build the graph, run the census, free the graph."""
     g = tc_graph_create(n, src, dst, device=device)

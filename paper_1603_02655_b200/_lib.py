@@ -73,6 +73,7 @@ _SIGS = {
     "tc_profile_enable": (cint, [vp, cint]),
     "tc_profile_get": (cint, [vp, ctypes.POINTER(tc_profile)]),
     "tc_launch_count": (u64, [vp]),
+    "tc_trim_memory": (cint, []),
     "tc_read_arcs": (cint, [ctypes.c_char_p, cint, cint, u64p, ctypes.POINTER(u32p),
                             ctypes.POINTER(u32p), u64p]),
     "tc_free_arcs": (None, [u32p]),

@@ -201,6 +201,28 @@ using namespace tc;
 extern "C" {
 
 const char *tc_last_error(void) { return g_err.c_str(); }
+
+tc_status tc_trim_memory(void) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_cache) {
+        cudaSetDevice(kv.first.dev);
+        for (void *q : kv.second) cudaFreeAsync(q, kv.first.stream);
+    }
+    g_cache.clear();
+    g_cached = 0;
+    int ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    for (int d = 0; d < ndev; d++) {
+        cudaSetDevice(d);
+        cudaDeviceSynchronize();
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+    }
+    cudaSetDevice(cur);
+    return TC_OK;
+}
 int tc_abi_version(void) { return TC_ABI_VERSION; }
 
 tc_status tc_close_census(uint64_t n, uint64_t counts[16], uint64_t *c003_hi) {

@@ -410,3 +410,25 @@ def test_row_sort_lengths_vs_oracle(tcb, lengths):
         g = oracle.Graph(a.n, a.src, a.dst)
         assert c == g.census(), (lengths, seed)
         assert st == g.stats(), (lengths, seed)
+
+
+def test_default_allocator_cache_and_trim(tcb):
+    """The default allocator (exact-size block cache, abi.cu) reuses a freed
+    graph's blocks for the next graph of the same size on the same stream;
+    tc_trim_memory returns them to the driver; the census is unchanged
+    through both (and with the torch allocator)."""
+    a = synth.random_digraph(2000, 0.004, seed=77, dups=3)
+    exp = oracle.census(a.n, a.src, a.dst)
+    for torch_alloc in (False, True):
+        for _ in range(3):
+            g = tcb.tc_graph_create(a.n, a.src, a.dst, use_torch_allocator=torch_alloc)
+            try:
+                assert g.census() == exp
+            finally:
+                g.close()
+        tcb.tc_trim_memory()
+    g = tcb.tc_graph_create(a.n, a.src, a.dst, use_torch_allocator=False)
+    try:
+        assert g.census() == exp and g.stats()["dyads"] > 0
+    finally:
+        g.close()
