@@ -2,7 +2,7 @@
 # C2, C4, C5, C3 64-type, reference arm), ncu launch lists and --set full
 # captures of the census kernels and the build kernels -> gpurun_out/
 mkdir -p gpurun_out
-O=gpurun_out/fin2
+O=gpurun_out/fin3
 mkdir -p $O
 rm -f /tmp/tc_arcs_*.npz
 (nproc; lscpu | head -20; free -g; nvidia-smi) > $O/box.txt 2>&1
