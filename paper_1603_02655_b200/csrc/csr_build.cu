@@ -260,7 +260,7 @@ k_row_classify(const uint32_t *__restrict__ rstart, const uint32_t *__restrict__
 // in registers (the row key is the same for all)
 template <int P>
 __device__ __forceinline__ void sort_row_regs(uint64_t *__restrict__ X, uint32_t u, uint32_t s0,
-                                              uint32_t len) {
+                                              uint32_t len, unsigned long long *dupf) {
     uint32_t v[P];
 #pragma unroll
     for (int j = 0; j < P; j++) v[j] = j < (int)len ? (uint32_t)__ldg(X + s0 + j) : ~0u;
@@ -281,18 +281,25 @@ __device__ __forceinline__ void sort_row_regs(uint64_t *__restrict__ X, uint32_t
         }
     }
     const uint64_t hi = (uint64_t)u << 32;
+    bool dup = false;   // two keys of one (row, max): a duplicate arc or a mutual pair
 #pragma unroll
-    for (int j = 0; j < P; j++)
+    for (int j = 0; j < P; j++) {
         if (j < (int)len) X[s0 + j] = hi | v[j];
+        if (j + 1 < P) dup |= j + 1 < (int)len && (v[j] >> 2) == (v[j + 1] >> 2);
+    }
+    if (dup) atomicOr(dupf, 1ull);
 }
 
 // classes 0..2 (rows of 2..32 keys) in one launch: block b belongs to the
 // class whose block range holds it (class c has ceil(cnt[c] / 128) blocks)
 constexpr int kRssThreads = 128;
-__global__ void __launch_bounds__(kRssThreads)
+#ifndef TC_RSS_MINB
+#define TC_RSS_MINB 8
+#endif
+__global__ void __launch_bounds__(kRssThreads, TC_RSS_MINB)
 k_row_sort_small(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
                  const uint32_t *__restrict__ rend, const uint32_t *__restrict__ lists, uint64_t n,
-                 const unsigned long long *__restrict__ cnt) {
+                 const unsigned long long *__restrict__ cnt, unsigned long long *dupf) {
     uint64_t b = blockIdx.x;
     int c = 0;
     for (; c < 3; c++) {
@@ -305,9 +312,9 @@ k_row_sort_small(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
     if (i >= cnt[c]) return;
     const uint32_t u = __ldg(lists + (size_t)c * n + i);
     const uint32_t s0 = __ldg(rstart + u), len = __ldg(rend + u) - s0;
-    if (c == 0) sort_row_regs<8>(X, u, s0, len);
-    else if (c == 1) sort_row_regs<16>(X, u, s0, len);
-    else sort_row_regs<32>(X, u, s0, len);
+    if (c == 0) sort_row_regs<8>(X, u, s0, len, dupf);
+    else if (c == 1) sort_row_regs<16>(X, u, s0, len, dupf);
+    else sort_row_regs<32>(X, u, s0, len, dupf);
 }
 
 // class 3 (33..64 keys): one warp per row, two elements per lane, bitonic
@@ -315,7 +322,7 @@ k_row_sort_small(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
 __global__ void __launch_bounds__(256)
 k_row_sort_w64(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
                const uint32_t *__restrict__ rend, const uint32_t *__restrict__ list,
-               const unsigned long long *__restrict__ cnt) {
+               const unsigned long long *__restrict__ cnt, unsigned long long *dupf) {
     const uint64_t nr = *cnt;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -346,6 +353,13 @@ k_row_sort_w64(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
         const uint64_t hi = (uint64_t)u << 32;
         if (lane < len) X[s0 + lane] = hi | e0;
         if (lane + 32 < len) X[s0 + 32 + lane] = hi | e1;
+        // duplicates: element i against element i + 1 (i = lane, lane + 32)
+        const uint32_t n0 = __shfl_down_sync(0xffffffffu, e0, 1), f1 = __shfl_sync(0xffffffffu, e1, 0);
+        const uint32_t n1 = __shfl_down_sync(0xffffffffu, e1, 1);
+        const uint32_t next0 = lane < 31 ? n0 : f1;
+        const bool dup = (lane + 1 < len && (e0 >> 2) == (next0 >> 2)) ||
+                         (lane < 31 && lane + 33 < len && (e1 >> 2) == (n1 >> 2));
+        if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(dupf, 1ull);
     }
 }
 
@@ -354,7 +368,7 @@ constexpr int kRswThreads = 256;
 __global__ void __launch_bounds__(kRswThreads)
 k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
                 const uint32_t *__restrict__ rend, const uint32_t *__restrict__ list,
-                const unsigned long long *__restrict__ cnt) {
+                const unsigned long long *__restrict__ cnt, unsigned long long *dupf) {
     __shared__ uint32_t buf[kRswThreads / 32][kRowMed];
     const uint64_t nr = *cnt;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -381,7 +395,12 @@ k_row_sort_warp(uint64_t *__restrict__ X, const uint32_t *__restrict__ rstart,
             }
         }
         const uint64_t hi = (uint64_t)u << 32;
-        for (uint32_t j = lane; j < len; j += 32) X[s0 + j] = hi | b[j];
+        bool dup = false;
+        for (uint32_t j = lane; j < len; j += 32) {
+            X[s0 + j] = hi | b[j];
+            dup |= j + 1 < len && (b[j] >> 2) == (b[j + 1] >> 2);
+        }
+        if (__any_sync(0xffffffffu, dup) && lane == 0) atomicOr(dupf, 1ull);
         __syncwarp();
     }
 }
@@ -421,10 +440,16 @@ __global__ void k_huge_rows(uint64_t *__restrict__ X, uint64_t *__restrict__ S,
 // pass 1: per warp (512 keys), number of run heads
 __global__ void __launch_bounds__(kHcThreads)
 k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
-             uint32_t *__restrict__ warp_tot) {
+             uint32_t *__restrict__ warp_tot, const unsigned long long *dupf) {
     const size_t L = m - *dropped;   // canonical keys (dropped arcs sort last)
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const size_t base = (size_t)blockIdx.x * kHcTile + (size_t)warp * 32 * kHcItems;
+    if (!*dupf) {   // the row sort saw no two keys of one (row, max): every key heads its run
+        if (lane == 0)
+            warp_tot[(size_t)blockIdx.x * kHcWarps + warp] =
+                (uint32_t)(base >= L ? 0 : min((size_t)(32 * kHcItems), L - base));
+        return;
+    }
     HeadChunk c;
     load_chunk(key, L, base, c);
     uint32_t nh = 0;
@@ -589,7 +614,10 @@ __global__ void k_offsets(const uint32_t *__restrict__ lo_start,
         if (u <= n) {
             const uint32_t o = lo_start[u] + up_start[u] + (uint32_t)u;
             off[u] = o;
-            if (u > 0) adj[o - 1] = 0xffffffffu;    // terminator of row u - 1
+            // terminator of row u - 1, if it has no upper entries (the rows
+            // with upper entries get theirs from k_upper_plan, next to their
+            // last entry)
+            if (u > 0 && up_start[u] == up_start[u - 1]) adj[o - 1] = 0xffffffffu;
             if (u < n) {
                 const uint32_t l1 = lo_start[u + 1], u1 = up_start[u + 1];
                 ups[u] = l1 + up_start[u] + (uint32_t)u;
@@ -700,7 +728,8 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
             // hub graph (more than a fifth of the keys in rows of > 64): the
             // full LSD (max bits, then min bits) from the arcs again is cheaper
             // than sorting the long rows (DESIGN 5.2)
-            unsigned long long init2[2] = {~0ull, 0};
+            // scratch[2] = 1: duplicates unknown (the head count reads the keys)
+            unsigned long long init2[3] = {~0ull, 0, 1};
             TC_CUDA(cudaMemcpyAsync(scratch.p, init2, sizeof(init2), cudaMemcpyHostToDevice, s));
             np = radix_passes_for(2, b, passes);
             np += radix_passes_for(32, b, passes + np);
@@ -709,18 +738,20 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
                 return st;
         } else {
             k_row_sort_small<<<(unsigned)(n / kRssThreads + 3), kRssThreads, 0, s>>>(
-                sorted, rstart, rend, lists.p, n, rc.p);
+                sorted, rstart, rend, lists.p, n, rc.p, scratch.p + 2);
             const uint64_t n33 = n < m / 33 ? n : m / 33;   // rows of >= 33 keys
             k_row_sort_w64<<<grid_for(n33 * 32, 256, 148 * 16), 256, 0, s>>>(
-                sorted, rstart, rend,
-                                                                       lists.p + 3 * n, rc.p + 3);
+                sorted, rstart, rend, lists.p + 3 * n, rc.p + 3, scratch.p + 2);
             k_row_sort_warp<<<148 * 7, kRswThreads, 0, s>>>(sorted, rstart, rend,
-                                                            lists.p + 4 * n, rc.p + 4);
+                                                            lists.p + 4 * n, rc.p + 4,
+                                                            scratch.p + 2);
             TC_CUDA(cudaGetLastError());
             g->launches += 3;
         }
         if (5 * rch[kRowClasses] <= m - dropped_h && rch[kRowClasses - 1]) {
             const uint64_t nh = rch[kRowClasses - 1];   // rows of > kRowMed keys
+            const unsigned long long one = 1;   // duplicates in these rows: not checked
+            TC_CUDA(cudaMemcpyAsync(scratch.p + 2, &one, sizeof(one), cudaMemcpyHostToDevice, s));
             const uint32_t *hl = lists.p + (size_t)(kRowClasses - 1) * n;
             const uint64_t ns = rch[kRowClasses + 1];
             DevBuf<uint32_t> hoff;
@@ -785,7 +816,8 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         const size_t ntiles = (m + kHcTile - 1) / kHcTile;
         DevBuf<uint32_t> wt;
         if ((st = wt.allocate(mem, ntiles * kHcWarps)) != TC_OK) return st;
-        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p);
+        k_head_count<<<(unsigned)ntiles, kHcThreads, 0, s>>>(sorted, m, scratch.p + 1, wt.p,
+                                                             scratch.p + 2);
         TC_CUDA(cudaGetLastError());
         st = scan_exclusive<uint32_t>(mem, ntiles * kHcWarps, ArrayIn<uint32_t>{wt.p},
                                       ArrayOutExcl<uint32_t>{wt.p}, total.p, s, &g->launches);

@@ -491,6 +491,9 @@ k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ 
                 continue;
             }
             I.adj[ls[j] + u[j] + (uint32_t)i] = e[j];
+            // the last upper entry of row u also writes the row's terminator
+            // (k_offsets writes it for rows without upper entries)
+            if (ls[j] + u[j] + (uint32_t)i + 2u == ou1[j]) I.adj[ou1[j] - 1] = 0xffffffffu;
             const uint32_t c = (ou1[j] - ou[j]) + (ov1[j] - ov[j]) - 2;
             const uint32_t t = (ou1[j] - 1 - up[j]) + (ov1[j] - 1 - pb[j]);
             I.dc[i] = c;
