@@ -16,7 +16,11 @@
 //                kRowMed): canonical pairs in the algorithm's own dyad order (u
 //                ascending, v ascending).  Rows of more than
 //                kRowMed keys are sorted together by one LSD (max bits, row
-//                bits) of their keys (k_huge_rows).
+//                bits) of their keys (k_huge_rows).  Hub graphs (more than a
+//                fifth of the keys in rows of > 64, known after one host read)
+//                take the full LSD (max bits, then min bits) instead.  The row
+//                sort also flags duplicate (row, max) keys; without any, the
+//                run-head count below skips reading the keys.
 //   3. compact   a ballot/popc compaction keeps the first key of each (min,
 //                max) run with the OR of the run's direction bits (dedup +
 //                mutual merge): the canonical dyad list dyad_u / dyad_e (the
