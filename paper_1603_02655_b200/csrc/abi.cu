@@ -97,10 +97,17 @@ void *Mem::alloc(size_t bytes) {
         // reservations back to the driver, and retry once (a request larger
         // than any free chunk needs fresh physical memory)
         std::lock_guard<std::mutex> lk(g_cache_mu);
-        for (auto &kv : g_cache)
-            for (void *q : kv.second) cudaFreeAsync(q, kv.first.stream);
-        g_cache.clear();
-        g_cached = 0;
+        for (auto it2 = g_cache.begin(); it2 != g_cache.end();) {
+            if (it2->first.dev != dev) {   // other devices' blocks stay cached
+                ++it2;
+                continue;
+            }
+            for (void *q : it2->second) {
+                cudaFreeAsync(q, it2->first.stream);
+                g_cached -= it2->first.bytes;
+            }
+            it2 = g_cache.erase(it2);
+        }
         cudaDeviceSynchronize();
         cudaMemPool_t pool;
         if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);

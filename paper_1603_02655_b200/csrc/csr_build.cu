@@ -916,6 +916,15 @@ tc_status build_finish(tc_graph *g, const unsigned long long *h, uint32_t D) {
     const uint64_t loops = h[1];
     const uint64_t nnz = 2ull * D;
     g->adj_n = nnz + n + 8;
+    // the stats first: a failed tag prefix below leaves a graph whose big
+    // dyads are merged instead of searched (same census)
+    g->st.loops_dropped = loops;
+    g->st.dyads = D;
+    g->st.sum_deg_sq = h[4];
+    g->st.max_degree = h[5];
+    g->st.m = h[6];
+    g->st.mutual_dyads = h[7];
+    g->st.dups_dropped = m - loops - h[6];
     // 7. tag prefix counts for the skewed-pair path (hub graphs only)
     if (h[5] >= kSparseMinDegree) {
         Mem &mem = g->mem;
@@ -926,21 +935,16 @@ tc_status build_finish(tc_graph *g, const unsigned long long *h, uint32_t D) {
             set_error("device allocation for the tag prefix failed");
             return TC_E_OOM;
         }
-        g->tagpre = tp;
-        g->tagpre_n = nt + 1;
         tc_status st;
         if ((st = scan_exclusive<uint64_t>(mem, nt, TagIn{g->adj}, ArrayOutExcl<uint64_t>{tp},
-                                           tp + nt, s, &g->launches)) != TC_OK)
+                                           tp + nt, s, &g->launches)) != TC_OK) {
+            mem.free(tp, (nt + 1) * sizeof(uint64_t));
             return st;
+        }
         TC_CUDA(cudaStreamSynchronize(s));
+        g->tagpre = tp;   // published only once complete
+        g->tagpre_n = nt + 1;
     }
-    g->st.loops_dropped = loops;
-    g->st.dyads = D;
-    g->st.sum_deg_sq = h[4];
-    g->st.max_degree = h[5];
-    g->st.m = h[6];
-    g->st.mutual_dyads = h[7];
-    g->st.dups_dropped = m - loops - h[6];
     return TC_OK;
 }
 
