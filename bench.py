@@ -445,12 +445,12 @@ def run_ours(args):
     trips = int(profs[-1]["bin_work"][2 + dom])
     touched = 4.0 * (trips + (sp_units if dom == 1 else 0)) + 24.0 * items
     # a1 build: compulsory bytes (read the arcs once, write the CSR, the five
-    # dyad arrays, off and ups) and the sort traffic of the passes it runs
-    nb = max(1, int(np.ceil(np.log2(max(a.n, 2)))))
-    passes_m, passes_d = 2 * ((nb + 7) // 8), (nb + 7) // 8
+    # dyad arrays, off and ups) and the sort traffic of the passes the build
+    # reports it ran (tc_profile.build_sort)
+    passes_m, passes_d, row_keys, huge_kp = profs[-1]["build_sort"]
     m_, d_ = stats["m_in"], stats["dyads"]
     compulsory = 8.0 * m_ + 4.0 * (2 * d_ + a.n) + 20.0 * d_ + 8.0 * a.n
-    sort_bytes = 24.0 * (passes_m * m_ + passes_d * d_)
+    sort_bytes = 24.0 * (passes_m * m_ + passes_d * d_ + huge_kp) + 16.0 * row_keys
     census_ms = float(np.mean([p["census_ms"] for p in profs]))
     plan_ms = float(np.mean([p["plan_ms"] for p in profs]))
     build_ms = float(np.mean([p["build_ms"] for p in profs]))
@@ -490,12 +490,15 @@ def run_ours(args):
                 "bound": "hbm", "build_ms": build_ms, "peak": hbm, "unit": "GB/s",
                 "compulsory_bytes": compulsory,
                 "compulsory_frac": (compulsory / (build_ms * 1e-3) / 1e9) / hbm,
-                "sort_passes": {"over_m_keys": passes_m, "over_D_keys": passes_d},
+                "sort_passes": {"over_m_keys": passes_m, "over_D_keys": passes_d,
+                                "row_network_keys": row_keys,
+                                "long_row_lsd_key_passes": huge_kp},
                 "sort_bytes": sort_bytes,
                 "sort_gbps_if_all_time": sort_bytes / (build_ms * 1e-3) / 1e9,
                 "model": "compulsory = 8m (arcs) + 4(2D+n) (adj) + 20D (dyad arrays) + 8n "
                          "(off, ups); sort = 24 B per key per LSD pass (upsweep read + "
-                         "downsweep read + write)"},
+                         "downsweep read + write) + 16 B per key left to the per-row "
+                         "networks (read + write)"},
             "e2e": {"value": m_arcs * args.steps / (e2e_total * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": 8 * a_m, "d2h_bytes_per_step": 320},
             "gpu_launches": launches_total,

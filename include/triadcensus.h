@@ -118,6 +118,12 @@ typedef struct {
     uint64_t sparse_sum_c;  /* skewed-pair dyads: sum of |N(u)|+|N(v)| (part of bin_work[1]) */
     uint64_t sparse_units;  /* skewed-pair dyads: entries they read = sum over dyads of
                                s * ceil(log2(l + 1)) + 4 (s, l: short and long list) */
+    uint64_t build_sort[4]; /* a1, the graph's build (filled whether or not profiling is
+                               on): [0] LSD passes over the m arc keys, [1] LSD passes
+                               over the D transposed keys, [2] keys in rows of at most
+                               1024 keys left to the per-row networks (0 when the build
+                               took the full LSD: hub graphs), [3] key-passes of the
+                               composite LSD over the rows longer than that */
 } tc_profile;
 
 /* Build the device graph from an arc list (a1).

@@ -94,7 +94,8 @@ class Graph:
         return {"build_ms": p.build_ms, "plan_ms": p.plan_ms, "census_ms": p.census_ms,
                 "kernel_ms": list(p.kernel_ms), "bin_items": [int(x) for x in p.bin_items],
                 "bin_work": [int(x) for x in p.bin_work], "sparse_sum_c": int(p.sparse_sum_c),
-                "sparse_units": int(p.sparse_units)}
+                "sparse_units": int(p.sparse_units),
+                "build_sort": [int(x) for x in p.build_sort]}
 
     def launches(self) -> int:
         return int(lib.tc_launch_count(self._h))

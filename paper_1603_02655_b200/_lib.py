@@ -45,7 +45,7 @@ class tc_profile(ctypes.Structure):
     _fields_ = [("build_ms", ctypes.c_float), ("plan_ms", ctypes.c_float),
                 ("census_ms", ctypes.c_float), ("kernel_ms", ctypes.c_float * 4),
                 ("bin_items", u64 * 4), ("bin_work", u64 * 4), ("sparse_sum_c", u64),
-                ("sparse_units", u64)]
+                ("sparse_units", u64), ("build_sort", u64 * 4)]
 
 
 TC_OK, TC_E_INVALID, TC_E_RANGE, TC_E_OOM, TC_E_CUDA, TC_E_NCCL, TC_E_OVERFLOW = range(7)

@@ -405,6 +405,7 @@ tc_status tc_profile_get(const tc_graph *g, tc_profile *out) {
     if (tc_status fs = graph_finalize(g)) return fs;
     std::lock_guard<std::mutex> lk(g->mu);
     *out = g->prof;
+    for (int i = 0; i < 4; i++) out->build_sort[i] = g->build_sort[i];
     return TC_OK;
 }
 

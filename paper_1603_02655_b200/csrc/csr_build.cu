@@ -536,12 +536,34 @@ constexpr int kWlBatch = 4;
 #ifndef TC_WL_PARTS
 #define TC_WL_PARTS 1
 #endif
+// TC_WL_HINT: L2 cache hints.  1 = the sorted keys and the adj stores
+// stream (evict-first); 2 = also the random ul[k] read-modify-write carries
+// an evict_last policy, so the D-word array stays in L2 while the 8-byte
+// keys stream past it and its partially written sectors are not written
+// back and re-fetched
+#ifndef TC_WL_HINT
+#define TC_WL_HINT 0
+#endif
+#if TC_WL_HINT >= 2
+__device__ __forceinline__ uint32_t wl_ld_keep(const uint32_t *p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void wl_st_keep(uint32_t *p, uint32_t v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" :: "l"(p), "r"(v), "l"(pol) : "memory");
+}
+#endif
 __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *__restrict__ dD,
                               const uint32_t *__restrict__ up_start, uint32_t *__restrict__ adj,
                               uint32_t *__restrict__ ul, uint32_t *__restrict__ lo_start,
                               uint32_t klo, uint32_t khi, int starts) {
     const size_t D = *dD;
     const size_t stride = (size_t)gridDim.x * blockDim.x;
+#if TC_WL_HINT >= 2
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#endif
     for (size_t i0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < D;
          i0 += kWlBatch * stride) {
         uint64_t key[kWlBatch], prv[kWlBatch];
@@ -549,8 +571,13 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *_
 #pragma unroll
         for (int j = 0; j < kWlBatch; j++) {
             const size_t i = i0 + j * stride;
+#if TC_WL_HINT >= 1
+            key[j] = i < D ? __ldcs(tk + i) : 0ull;
+            prv[j] = (i < D && i) ? __ldcs(tk + i - 1) : ~0ull;
+#else
             key[j] = i < D ? __ldg(tk + i) : 0ull;
             prv[j] = (i < D && i) ? __ldg(tk + i - 1) : ~0ull;
+#endif
         }
 #pragma unroll
         for (int j = 0; j < kWlBatch; j++) {
@@ -558,7 +585,11 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *_
             const uint32_t k = (uint32_t)key[j];
             const bool mine = i < D && k >= klo && k < khi;
             us[j] = mine ? __ldg(up_start + key_row(key[j])) : 0u;
+#if TC_WL_HINT >= 2
+            val[j] = mine ? wl_ld_keep(ul + k, pol) : 0u;
+#else
             val[j] = mine ? ul[k] : 0u;
+#endif
         }
 #pragma unroll
         for (int j = 0; j < kWlBatch; j++) {
@@ -567,8 +598,16 @@ __global__ void k_write_lower(const uint64_t *__restrict__ tk, const uint32_t *_
             const uint32_t r = key_row(key[j]), k = (uint32_t)key[j];
             if (k >= klo && k < khi) {
                 const uint32_t pos = us[j] + r + (uint32_t)i;
+#if TC_WL_HINT >= 1
+                __stcs(adj + pos, val[j]);
+#else
                 adj[pos] = val[j];
+#endif
+#if TC_WL_HINT >= 2
+                wl_st_keep(ul + k, pos + 1u, pol);
+#else
                 ul[k] = pos + 1u;
+#endif
             }
             const uint32_t prev = i ? key_row(prv[j]) : 0xffffffffu;
             if (starts && (i == 0 || prev != r)) {
@@ -703,6 +742,7 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
         if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
                                  &as)) != TC_OK)
             return st;
+        g->build_sort[0] = (uint64_t)np;
         // row sort, in place in `sorted`
         DevBuf<uint32_t> rb, lists;
         DevBuf<unsigned long long> rc;
@@ -740,7 +780,9 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
             if ((st = radix_sort_u64(mem, keys.p, tmp.p, m, passes, np, s, &g->launches, &sorted,
                                      &as)) != TC_OK)
                 return st;
+            g->build_sort[0] += (uint64_t)np;
         } else {
+            g->build_sort[2] = m - dropped_h - rch[kRowClasses + 1];
             k_row_sort_small<<<(unsigned)(n / kRssThreads + 3), kRssThreads, 0, s>>>(
                 sorted, rstart, rend, lists.p, n, rc.p, scratch.p + 2);
             const uint64_t n33 = n < m / 33 ? n : m / 33;   // rows of >= 33 keys
@@ -777,6 +819,7 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
             if ((st = radix_sort_u64(mem, S.p, S2.p, ns, passes, np, s, &g->launches, &ss)) !=
                 TC_OK)
                 return st;
+            g->build_sort[3] = ns * (uint64_t)np;
             k_huge_rows<false><<<gh, 256, 0, s>>>(sorted, ss, rstart, hl, hoff.p, nh, ns);
             TC_CUDA(cudaGetLastError());
             g->launches += 2;
@@ -866,6 +909,7 @@ tc_status build_csr(tc_graph *g, const uint32_t *d_src, const uint32_t *d_dst, u
     if ((st = radix_sort_u64(mem, spare, tother, Dub, rpasses, nrp, s, &g->launches, &tsorted,
                              nullptr, total.p)) != TC_OK)
         return st;
+    g->build_sort[1] = Dub ? (uint64_t)nrp : 0;
     // 5. assemble the symmetric rows: lower entries (+ lo_start, dyad_pb),
     // then offsets, sentinels and vertex stats, then upper entries
     uint32_t *adj = (uint32_t *)mem.alloc((2ull * Dub + n + 8) * sizeof(uint32_t));

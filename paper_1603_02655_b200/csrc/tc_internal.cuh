@@ -124,6 +124,7 @@ struct tc_graph {
     // of a row range with two loads instead of a merge (census.cu)
     uint64_t *tagpre = nullptr; size_t tagpre_n = 0;
     size_t adj_alloc_n = 0;             // entries allocated for adj (>= adj_n)
+    uint64_t build_sort[4] = {0, 0, 0, 0};   // tc_profile.build_sort (csr_build.cu)
     // lazy end of the build: the stats and D are copied into a pinned slot
     // and `ready` is recorded; the first call that needs the host-side stats
     // waits there (graph_finalize), so the caller's own host work between

@@ -412,6 +412,38 @@ def test_row_sort_lengths_vs_oracle(tcb, lengths):
         assert st == g.stats(), (lengths, seed)
 
 
+def test_build_sort_report(tcb):
+    """tc_profile.build_sort names the a1 path the build took: a graph with
+    short rows takes ceil(b / 8) LSD passes on the row bits plus the per-row
+    networks (every canonical key of a row of <= 1024 keys); a graph with one
+    1025-key row adds the composite LSD over that row; a hub graph (more than
+    a fifth of the keys in rows of > 64 keys) takes the full LSD and no
+    networks.  The transposed sort is ceil(b / 8) passes either way."""
+    n = 3000
+    b = int(np.ceil(np.log2(n)))
+    passes = (b + 7) // 8
+    cases = [(_row_lengths_graph([31, 33, 64, 65], n, 0), "rows"),
+             (_row_lengths_graph([1025, 40], n, 1), "huge"),
+             (synth.out_star(n - 1), "hub")]
+    for a, kind in cases:
+        g = tcb.tc_graph_create(a.n, a.src, a.dst)
+        try:
+            bs = g.profile_get()["build_sort"]
+            st = g.stats()
+        finally:
+            g.close()
+        assert bs[1] == passes, (kind, bs)
+        keys = st["m_in"] - st["loops_dropped"]
+        if kind == "hub":
+            assert bs[0] == 3 * passes, (kind, bs)     # the row-bit passes, then max + min bits
+            assert bs[2] == 0 and bs[3] == 0, (kind, bs)
+        else:
+            assert bs[0] == passes, (kind, bs)
+            huge = 1025 if kind == "huge" else 0
+            assert bs[2] == keys - huge, (kind, bs, keys)
+            assert (bs[3] > 0) == (kind == "huge"), (kind, bs)
+
+
 def test_default_allocator_cache_and_trim(tcb):
     """The default allocator (exact-size block cache, abi.cu) reuses a freed
     graph's blocks for the next graph of the same size on the same stream;
