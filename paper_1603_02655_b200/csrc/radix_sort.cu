@@ -22,7 +22,13 @@ namespace tc {
 namespace {
 
 constexpr int kRsThreads = 256;                  // upsweep
-constexpr int kRsItems = 16;
+#ifndef TC_RS_ITEMS
+#define TC_RS_ITEMS 16
+#endif
+#ifndef TC_DS_MINB
+#define TC_DS_MINB 4
+#endif
+constexpr int kRsItems = TC_RS_ITEMS;
 constexpr int kRsTile = kRsThreads * kRsItems;   // 4096 keys per block
 constexpr int kDsThreads = 256;                  // downsweep: 16 keys per thread,
 constexpr int kDsWarps = kDsThreads / 32;        // no register spills
@@ -170,7 +176,7 @@ __device__ __forceinline__ void ds_load_rank(const uint64_t *__restrict__ keys, 
 }
 
 template <int BITS, bool ARCS>
-__global__ void __launch_bounds__(kDsThreads, 4)
+__global__ void __launch_bounds__(kDsThreads, TC_DS_MINB)
 rs_downsweep(const uint64_t *__restrict__ keys, uint64_t *__restrict__ out, size_t n, int shift,
              uint32_t mask, int radix, const uint32_t *__restrict__ offs, size_t ntiles,
              const uint32_t *__restrict__ totals, ArcSource a, const uint32_t *dn) {
