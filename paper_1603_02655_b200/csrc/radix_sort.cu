@@ -160,11 +160,7 @@ __device__ __forceinline__ void ds_load_rank(const uint64_t *__restrict__ keys, 
         // lanes holding the same digit: intersect one ballot per digit bit
         // (cheaper than __match_any_sync on sm_100)
         uint32_t peers = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bit = 0; bit < BITS; bit++) {   // only the digit's own bits
-            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-            peers &= ((d >> bit) & 1u) ? b : ~b;
-        }
+        peers &= warp_peers<BITS>(d);   // only the digit's own bits
         uint32_t r = 0;
         if (valid) r = wc[d] + __popc(peers & lt);
         __syncwarp();

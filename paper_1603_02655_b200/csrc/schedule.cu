@@ -98,12 +98,7 @@ k_plan_tile(const PlanIn P, uint64_t N, uint64_t n, BinItemT *__restrict__ tl,
         cst[k] = valid ? __ldg(P.dt + i) : 0u;
         uint32_t d = valid ? digit_of(cst[k]) : 0x10000u;
         // lanes holding the same digit: one ballot per digit bit
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bit = 0; bit < 8; bit++) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-            peers &= ((d >> bit) & 1u) ? b : ~b;
-        }
+        const uint32_t peers = __ballot_sync(0xffffffffu, valid) & warp_peers<8>(d);
         uint32_t r = 0;
         if (valid) r = wc[warp][d] + __popc(peers & lt);
         __syncwarp();
@@ -520,12 +515,7 @@ k_upper_plan(const UpperIn I, BinItemT *__restrict__ tl, uint32_t *__restrict__ 
         const uint64_t i = tile0 + wbase + k * 32 + lane;
         const bool valid = i < N;
         const uint32_t d = valid ? (uint32_t)dgs[wbase + k * 32 + lane] : 0x10000u;
-        uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-        for (int bit = 0; bit < 8; bit++) {
-            const uint32_t b = __ballot_sync(0xffffffffu, (d >> bit) & 1u);
-            peers &= ((d >> bit) & 1u) ? b : ~b;
-        }
+        const uint32_t peers = __ballot_sync(0xffffffffu, valid) & warp_peers<8>(d);
         uint32_t r = 0;
         if (valid) r = wc[warp][d] + __popc(peers & lt);
         __syncwarp();

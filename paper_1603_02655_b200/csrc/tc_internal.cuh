@@ -102,6 +102,31 @@ struct BinItemW {   // warp bin: dyad index (in the planned range), diagonals [d
     uint32_t k, d0, d1, pad;
 };
 
+#ifdef __CUDACC__
+// Lanes of the (full) warp whose value d agrees with mine on bits [0, BITS):
+// one ballot per bit, each bit tested once -- the predicate feeds both the
+// ballot and the lane's own mask (peers &= bit ? b : ~b as one XNOR).  The
+// plain C form tests the bit twice (7 instructions per bit, 4 here; the LSD
+// downsweep 96 -> 82 us per pass at C3).  Callers AND the result with the
+// lanes that hold a valid d.
+template <int BITS>
+__device__ __forceinline__ uint32_t warp_peers(uint32_t d) {
+    uint32_t peers = 0xffffffffu;
+#pragma unroll
+    for (int bit = 0; bit < BITS; bit++) {
+        uint32_t b, msk;
+        asm("{\n\t.reg .pred p;\n\t.reg .b32 t;\n\t"
+            "and.b32 t, %2, %3;\n\tsetp.ne.u32 p, t, 0;\n\t"
+            "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t"
+            "selp.b32 %1, -1, 0, p;\n\t}"
+            : "=r"(b), "=r"(msk)
+            : "r"(d), "r"(1u << bit));
+        peers &= ~(b ^ msk);
+    }
+    return peers;
+}
+#endif
+
 }  // namespace tc
 
 // the opaque graph
