@@ -59,17 +59,48 @@ rs_upsweep(const uint64_t *__restrict__ keys, size_t n, int shift, uint32_t mask
     const size_t base = (size_t)blockIdx.x * kRsTile;
     if (ARCS) {
         unsigned long long dropped = 0;
-#pragma unroll 4
-        for (int k = 0; k < kRsItems; k++) {
-            const size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
-            if (i < n) {
-                const uint32_t sv = __ldg(a.src + i), dv = __ldg(a.dst + i);
-                const uint64_t key = arc_key(sv, dv, a.nv);
-                if (key == ~0ull) {
-                    dropped++;
-                    if (sv >= a.nv || dv >= a.nv) atomicMin(&a.scratch[0], (unsigned long long)i);
+        if (base + kRsTile <= n &&
+            ((reinterpret_cast<uintptr_t>(a.src) | reinterpret_cast<uintptr_t>(a.dst)) & 15u) == 0) {
+            // full tile of 16-byte-aligned arc arrays: 4 arcs per load, all
+            // loads in flight before the first count (as the key path)
+            const uint4 *s4 = reinterpret_cast<const uint4 *>(a.src + base);
+            const uint4 *d4 = reinterpret_cast<const uint4 *>(a.dst + base);
+            uint4 sv[kRsItems / 4], dv[kRsItems / 4];
+#pragma unroll
+            for (int k = 0; k < kRsItems / 4; k++) {
+                sv[k] = __ldcs(s4 + k * kRsThreads + threadIdx.x);
+                dv[k] = __ldcs(d4 + k * kRsThreads + threadIdx.x);
+            }
+#pragma unroll
+            for (int k = 0; k < kRsItems / 4; k++) {
+                const uint32_t ss[4] = {sv[k].x, sv[k].y, sv[k].z, sv[k].w};
+                const uint32_t dd[4] = {dv[k].x, dv[k].y, dv[k].z, dv[k].w};
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const uint64_t key = arc_key(ss[j], dd[j], a.nv);
+                    if (key == ~0ull) {
+                        dropped++;
+                        if (ss[j] >= a.nv || dd[j] >= a.nv)
+                            atomicMin(&a.scratch[0], (unsigned long long)(
+                                base + 4 * ((size_t)k * kRsThreads + threadIdx.x) + j));
+                    }
+                    atomicAdd(&h[(uint32_t)(key >> shift) & mask], 1u);
                 }
-                atomicAdd(&h[(uint32_t)(key >> shift) & mask], 1u);
+            }
+        } else {
+#pragma unroll 4
+            for (int k = 0; k < kRsItems; k++) {
+                const size_t i = base + (size_t)k * kRsThreads + threadIdx.x;
+                if (i < n) {
+                    const uint32_t sv = __ldg(a.src + i), dv = __ldg(a.dst + i);
+                    const uint64_t key = arc_key(sv, dv, a.nv);
+                    if (key == ~0ull) {
+                        dropped++;
+                        if (sv >= a.nv || dv >= a.nv)
+                            atomicMin(&a.scratch[0], (unsigned long long)i);
+                    }
+                    atomicAdd(&h[(uint32_t)(key >> shift) & mask], 1u);
+                }
             }
         }
         for (int o = 16; o; o >>= 1) dropped += __shfl_xor_sync(0xffffffffu, dropped, o);

@@ -195,6 +195,44 @@ def test_device_arcs_equal_host_arcs(tcb):
     g.close()
 
 
+def test_device_arcs_any_alignment(tcb):
+    """The first sort pass reads the arc arrays with 16-byte loads when both
+    are 16-byte aligned and per arc otherwise (radix_sort.cu rs_upsweep):
+    arrays starting 0..3 elements into an allocation give the same census
+    and stats as the host path."""
+    import torch
+    a = synth.make_config("C2")
+    m = a.src.size
+    exp = gpu_census(tcb, a)
+
+    def at(x, off):   # x on the device, starting `off` int32 into a fresh allocation
+        buf = torch.zeros(m + 4, dtype=torch.int32, device="cuda")
+        buf[off:off + m] = torch.from_numpy(x.astype(np.int32)).cuda()
+        return buf[off:off + m]
+    for off_s, off_d in ((0, 0), (1, 0), (0, 2), (3, 3)):
+        g = tcb.tc_graph_create(a.n, at(a.src, off_s), at(a.dst, off_d))
+        try:
+            assert (g.census(), g.stats()) == exp, (off_s, off_d)
+        finally:
+            g.close()
+
+
+def test_out_of_range_arc_index_full_tiles(tcb):
+    """The smallest index of an out-of-range arc is reported from full
+    4096-arc tiles as well as from the partial last tile."""
+    rng = np.random.default_rng(5)
+    n, m = 1000, 20000
+    src = rng.integers(0, n, m).astype(np.uint32)
+    dst = rng.integers(0, n, m).astype(np.uint32)
+    src[7001] = n + 5
+    dst[5003] = n
+    with pytest.raises(tcb.TCError, match="arc 5003 "):
+        tcb.tc_graph_create(n, src, dst)
+    src[5] = 2**31   # one more, in the first tile
+    with pytest.raises(tcb.TCError, match="arc 5 "):
+        tcb.tc_graph_create(n, src, dst)
+
+
 def test_closed_form_hub_star_warp_bin_and_high_word(tcb):
     # cost 2e5+1 per dyad -> warp-bin items (skewed pairs); n = 1e7 -> 003
     # needs the high word
