@@ -466,10 +466,13 @@ k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
     if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = nh;
 }
 
+#ifndef TC_HW_MINB
+#define TC_HW_MINB 1
+#endif
 // pass 2: canonical dyad list, transposed keys (row v, dyad index k), the
 // lower entry of each dyad (ul[k] = u<<2 | swapped tag) and up_start at row
 // changes (warp_off = exclusive scan of pass 1's per-warp counts)
-__global__ void __launch_bounds__(kHcThreads)
+__global__ void __launch_bounds__(kHcThreads, TC_HW_MINB)
 k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
              const uint32_t *__restrict__ warp_off,
              uint32_t *__restrict__ du, uint32_t *__restrict__ de, uint64_t *__restrict__ tk,
