@@ -466,13 +466,16 @@ k_head_count(const uint64_t *__restrict__ key, size_t m, const unsigned long lon
     if (lane == 0) warp_tot[(size_t)blockIdx.x * kHcWarps + warp] = nh;
 }
 
-#ifndef TC_HW_MINB
-#define TC_HW_MINB 1
-#endif
+// TC_HW_MINB: minimum blocks per SM for k_head_write (unset: plain
+// __launch_bounds__, 64 registers; an explicit 1 lets ptxas take 96)
 // pass 2: canonical dyad list, transposed keys (row v, dyad index k), the
 // lower entry of each dyad (ul[k] = u<<2 | swapped tag) and up_start at row
 // changes (warp_off = exclusive scan of pass 1's per-warp counts)
+#ifdef TC_HW_MINB
 __global__ void __launch_bounds__(kHcThreads, TC_HW_MINB)
+#else
+__global__ void __launch_bounds__(kHcThreads)
+#endif
 k_head_write(const uint64_t *__restrict__ key, size_t m, const unsigned long long *dropped,
              const uint32_t *__restrict__ warp_off,
              uint32_t *__restrict__ du, uint32_t *__restrict__ de, uint64_t *__restrict__ tk,
